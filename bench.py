@@ -1,0 +1,370 @@
+#!/usr/bin/env python
+"""Benchmark of the FP64 square-GEMM hot path (arXiv 2509.04594, tilebench).
+
+Metric (BASELINE.json): FP64 GFLOPS = (2N^3 - N^2) / kernel seconds at
+N = 10000, with % of B200 FP64 peak. One step = one C = A·B over the whole
+N x N problem (at N GPUs: B broadcast from rank 0 over NCCL + each rank's
+row-block GEMM).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--n 10000] [--impl ours|reference]
+
+Prints ONE JSON line on rank 0. Inputs (800 MB per matrix at N = 10000) are
+larger than the 126 MB L2, so no flush is needed between steps.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "FP64 GFLOPS ((2N^3−N^2)/kernel s) at N=10000; % of B200 FP64 peak"
+UNIT = "GFLOPS"
+SMS = 148
+FP64_FMA_PER_CLK_PER_SM = 64
+
+
+def flop_count(n: int) -> int:
+    return 2 * n**3 - n**2
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def measured_peaks() -> dict:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {}
+
+
+def fp64_peak_tflops() -> tuple[float, str]:
+    mhz = measured_peaks().get("sm_max_mhz")
+    src = "MEASURED_PEAKS.json sm_max_mhz"
+    if not mhz:
+        mhz, src = 1965.0, "B200_PROFILING.md clocks.max.sm"
+    return SMS * FP64_FMA_PER_CLK_PER_SM * 2 * mhz * 1e6 / 1e12, (
+        f"nominal FP64 (DMMA/DFMA pipe): 148 SM x 64 FMA/clk x 2 x {mhz:.0f} MHz ({src}); "
+        "measured DMMA register-only loop 37.15 TFLOPS (profiles/r01_pipe_microbench.txt)")
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling during the timed region (B200_PROFILING.md)."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        rows = []
+        try:
+            with open(self.path) as f:
+                for line in f:
+                    parts = [p.strip() for p in line.split(",")]
+                    if len(parts) >= 9:
+                        rows.append(parts)
+        except OSError:
+            pass
+        finally:
+            if self.path:
+                try:
+                    os.unlink(self.path)
+                except OSError:
+                    pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        sm = [num(r[1]) for r in rows if num(r[1])]
+        mx = max((num(r[2]) or 0) for r in rows)
+        power = [num(r[3]) for r in rows if num(r[3])]
+        load = [s for s, r in zip(sm, rows) if (num(r[3]) or 0) > 300] or sm
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(rows), "power_w_max": max(power) if power else None}
+
+
+def cpu_sample(n: int, threads: int, target_s: float, seed_a: int = 1, seed_b: int = 2) -> dict:
+    """The reference's CPU tiled path (oracle C port of tile_range_kernel +
+    plan_partitions, pthreads) timed on a bounded row sample of the N x N
+    workload; rows of tiled(A[rows], B) are bitwise rows of the full product."""
+    import numpy as np
+
+    from oracle import oracle as ref
+
+    rng = np.random.Generator(np.random.PCG64(seed_a))
+    b = rng.random((n, n)) * 3.0 + 2.0
+    rows = 16
+    while True:
+        a = np.random.Generator(np.random.PCG64(seed_b)).random((rows, n)) * 3.0 + 2.0
+        t0 = time.perf_counter()
+        ref.tiled_parallel(a, b, 32, threads)
+        dt = time.perf_counter() - t0
+        if dt >= target_s or rows >= n:
+            break
+        rows = min(n, max(rows * 2, int(rows * target_s / max(dt, 1e-3) * 1.05)))
+    flops = rows * (2 * n * n - n)
+    return {"value": flops / dt / 1e9, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"tiled-parallel K=32 (oracle/tb_oracle.c port of kernels.py:32-53 + backends.py:119-160) "
+                      f"on {rows} of {n} rows of the N={n} product, {dt:.1f} s, {threads} threads",
+            "seconds": dt}
+
+
+def run_reference(args) -> None:
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    vals = []
+    for i in range(args.warmup + args.steps):
+        s = cpu_sample(args.n, threads, target_s=args.ref_seconds)
+        if i >= args.warmup:
+            vals.append(s)
+    v = statistics.median([s["value"] for s in vals])
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic uniform[2,5] (numpy PCG64)",
+            "config": {"workload": f"N={args.n} FP64 square GEMM, bounded row sample on host cores", "n": args.n},
+            "cpu_baseline": {**{k: vals[-1][k] for k in ("unit", "cores", "kind", "sample")}, "value": v},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "ms_per_step": statistics.median([s["seconds"] for s in vals]) * 1e3}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args) -> None:
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2509_04594_b200 as tb
+    from paper_2509_04594_b200 import _lib
+    from paper_2509_04594_b200.multigpu import ShardedGemm, panel_bounds, row_partitions
+
+    rank, world, local = env_rank()
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}; launch N>1 under torchrun")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    n = args.n
+    parts = row_partitions(n, world)
+    r0, r1 = parts[rank]
+    g = torch.Generator(device=dev)
+    g.manual_seed(1000 + rank)
+    a_loc = torch.rand((r1 - r0, n), dtype=torch.float64, device=dev, generator=g) * 3.0 + 2.0
+    b = torch.empty((n, n), dtype=torch.float64, device=dev)
+    if rank == 0:
+        g.manual_seed(7)
+        b.copy_(torch.rand((n, n), dtype=torch.float64, device=dev, generator=g) * 3.0 + 2.0)
+    c_loc = torch.empty((r1 - r0, n), dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream()
+    sharded = ShardedGemm(panels=args.panels) if world > 1 else None
+
+    def step():
+        if world > 1:
+            sharded(a_loc, b, c_loc)
+        else:
+            tb.dgemm_launch(a_loc, b, c_loc, variant=args.variant)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    # kernel-only launch timing of the dominant kernel on its own stream (roofline achieved)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * args.steps)]
+    with ClockSampler(local) as clocks:
+        barrier()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for i in range(args.steps):
+            if world > 1:
+                step()
+            else:
+                ev[2 * i].record(stream)
+                step()
+                ev[2 * i + 1].record(stream)
+        t1.record(stream)
+        barrier()
+    total_s = t0.elapsed_time(t1) / 1e3
+    if world > 1:
+        t = torch.tensor([total_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_s = t.item()
+    ms_per_step = total_s / args.steps * 1e3
+    value = flop_count(n) * args.steps / total_s / 1e9
+    clk = clocks.summary()
+
+    # kernel-only per-launch durations (N=1: the timed launches themselves; N>1: a local-GEMM pass)
+    if world == 1:
+        launch_s = [ev[2 * i].elapsed_time(ev[2 * i + 1]) / 1e3 for i in range(args.steps)]
+    else:
+        launch_s = []
+        for _ in range(max(3, args.steps // 2)):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            tb.dgemm_launch(a_loc, b, c_loc)
+            e1.record(stream)
+            e1.synchronize()
+            launch_s.append(e0.elapsed_time(e1) / 1e3)
+    avg_launch = sum(launch_s) / len(launch_s)
+    flops_per_launch = (r1 - r0) * (2 * n * n - n)
+    peak, peak_src = fp64_peak_tflops()
+    achieved = flops_per_launch / avg_launch / 1e12
+    traffic = None
+    tr_path = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tr_path):
+        try:
+            traffic = json.load(open(tr_path)).get(str(n))
+        except (OSError, ValueError):
+            traffic = None
+
+    # cuBLAS DGEMM on the same buffers (reported baseline, not the target)
+    cub = []
+    for i in range(3 + 1):
+        _, sec = tb.cublas_dgemm(a_loc, b)
+        if i:
+            cub.append(sec)
+    cublas_gflops = flop_count(n) / world / min(cub) / 1e9 if cub else None
+
+    # correctness spot check of the timed result vs cuBLAS (normwise)
+    c_ref, _ = tb.cublas_dgemm(a_loc, b)
+    tb.dgemm_launch(a_loc, b, c_loc)
+    torch.cuda.synchronize()
+    rel = (torch.linalg.norm(c_loc - c_ref) / torch.linalg.norm(c_ref)).item()
+    del c_ref
+
+    # end to end through the reference-facing flat C ABI with pinned HOST buffers
+    a_h = a_loc.cpu().pin_memory()
+    b_h = b.cpu().pin_memory() if world == 1 else None
+    if world > 1:
+        dist.broadcast(b, 0)
+        b_h = b.cpu().pin_memory()
+    c_h = torch.empty((r1 - r0, n), dtype=torch.float64).pin_memory()
+    out_s = np.zeros(1)
+    e2e = np.zeros(1)
+    e2e_times = []
+    for i in range(1 + max(2, args.steps // 3)):
+        if world > 1:
+            dist.barrier()
+        st = tb.gpu_tiled_multiply_flat(local, a_h, b_h, r1 - r0, n, n, 32, c_h, out_s,
+                                        variant=args.variant, out_e2e_seconds=e2e)
+        if st != 0:
+            raise RuntimeError(f"flat ABI status {st}: {_lib.last_error()}")
+        if i:
+            e2e_times.append(e2e[0])
+    e2e_s = statistics.median(e2e_times)
+    if world > 1:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = t.item()
+    _lib.lib().tb_release()
+    h2d = 8 * n * n * world + 8 * n * n if world > 1 else 16 * n * n
+    d2h = 8 * n * n
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_sample(n, os.cpu_count() or 1, target_s=args.ref_seconds)
+        cpu.pop("seconds", None)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic uniform[2,5] (torch Philox on device; host e2e buffers copied from it)",
+            "config": {"workload": f"N={n} FP64 square GEMM C=A*B (BASELINE configs[3], 1..8 GPUs)", "n": n,
+                       "tile": "128x128x16 CTA, 8 DMMA warps + TMA producer warpgroup, 6 stages",
+                       "variant": args.variant, "parallelism": f"row-shard{world}" + (
+                           f" + NCCL broadcast of B ({args.panels} K-panels)" if world > 1 else ""),
+                       "l2": "inputs (800 MB/matrix) larger than L2; no flush"},
+            "pct_fp64_peak": 100.0 * value / 1e3 / peak,
+            "pct_fp64_peak_40tf": 100.0 * value / 1e3 / 40.0,
+            "cublas_gflops": cublas_gflops,
+            "vs_cublas": (value / world) / cublas_gflops if cublas_gflops else None,
+            "check_vs_cublas_normwise": rel,
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "dgemm_dmma_kernel<6, TMA>", "flops_per_launch": flops_per_launch,
+                         "avg_launch_ms": avg_launch * 1e3, "peak_source": peak_src},
+            "e2e": {"value": flop_count(n) / e2e_s / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h,
+                    "path": "tb_gpu_tiled_multiply_flat_ex (pinned host A,B -> H2D -> kernel -> D2H C), "
+                            "CUDA events on its stream"},
+            "gpu_launches": args.steps * (1 if world == 1 else len(panel_bounds(n, args.panels))),
+            "clocks": clk,
+            "cpu_baseline": cpu,
+            "library": _lib.version(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    p = argparse.ArgumentParser(description=__doc__.splitlines()[0])
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--n", type=int, default=10000)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--variant", default="auto")
+    p.add_argument("--panels", type=int, default=4, help="K-panels of the B broadcast at N>1")
+    p.add_argument("--ref-seconds", type=float, default=10.0, help="CPU sample length per measurement")
+    p.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = p.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,136 @@
+/*
+ * tbgpu.h — C ABI of the B200-native FP64 square-GEMM hot path
+ * (arXiv 2509.04594 "hand-rolled CUDA" tiled DGEMM, C = A·B).
+ *
+ * Drop-in boundary. The reference's binding surface for this path is the flat
+ * foreign-function-shaped entry of its GPU package,
+ *     gpuTiledMultiplyFlat(device, a, b, m, k, n, tileEdge, outC, outSeconds) -> status
+ *     (/root/reference/pkg/gpu/src/multiply.ts:54-79, status codes :49-52;
+ *      SPEC.md:453 "flat C-style interface ... out-parameters for result
+ *      buffer and device seconds"),
+ * registered into the Python harness as the `MultiplyFn` backend
+ * "gpu-tiled" (backends.py:56, :270-272; registry.ts:58-71).
+ * Every function below names the reference interface it replaces.
+ *
+ * Conventions
+ *  - All matrices are row-major float64 ("C-contiguous", matrices.py:1-5):
+ *    A is m x k (leading dim lda >= k), B is k x n (ldb >= n), C is m x n
+ *    (ldc >= n). C is fully overwritten unless `accumulate` is set.
+ *  - Device pointers (tb_dgemm*, tb_cublas_dgemm) come from the caller (in
+ *    this repo: torch CUDA tensors' data_ptr()); the library never allocates
+ *    caller-visible memory. Host pointers (tb_gpu_tiled_multiply_flat*) are
+ *    plain host buffers; the library stages them through a per-device cached
+ *    workspace, exactly as the reference executor copies to "device" buffers
+ *    before its kernel clock starts (executor.ts:92-104).
+ *  - Kernel seconds are kernel-only device time from CUDA events recorded on
+ *    the launching stream (executor.ts:104,144).
+ *  - Returns a TB_STATUS_* code; never throws, never aborts. On status != 0,
+ *    tb_last_error() gives a thread-local message.
+ */
+#ifndef TBGPU_H_
+#define TBGPU_H_
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define TB_API __attribute__((visibility("default")))
+#else
+#define TB_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes — multiply.ts:49-52 (0..3) plus 4 for CUDA/NCCL runtime errors. */
+#define TB_STATUS_OK 0
+#define TB_STATUS_BAD_DIMS 1
+#define TB_STATUS_OVER_LIMITS 2
+#define TB_STATUS_NO_DEVICE 3
+#define TB_STATUS_RUNTIME 4
+
+/* Kernel variants. AUTO picks DMMA_TMA when the TMA alignment rules hold
+ * (16-byte aligned bases and leading dims, i.e. even lda/ldb for float64)
+ * and DMMA_CPASYNC otherwise. PAPER is a faithful CUDA restatement of the
+ * reference's tiledKernelThread (kernel.ts:50-78): tile_edge x tile_edge
+ * threads, two shared tiles, running sum in k order, no FMA contraction —
+ * bitwise equal to the reference's naive oracle. */
+#define TB_VARIANT_AUTO 0
+#define TB_VARIANT_PAPER 1
+#define TB_VARIANT_DMMA_TMA 2
+#define TB_VARIANT_DMMA_CPASYNC 3
+#define TB_NUM_VARIANTS 4
+
+#define TB_DEFAULT_TILE_EDGE 32 /* limits.ts:40-42 */
+
+/* Replaces gpuTiledMultiplyFlat (multiply.ts:54-79) one for one: host
+ * buffers in, caller-owned outC (length out_c_len, must equal m*n, else
+ * BAD_DIMS as at multiply.ts:66) and outSeconds (kernel-only seconds).
+ * device < 0 or no CUDA device -> TB_STATUS_NO_DEVICE (multiply.ts:65).
+ * tile_edge follows validateLaunch (limits.ts:58-79): < 1 -> BAD_DIMS,
+ * tile_edge^2 > 1024 threads -> OVER_LIMITS. Uses TB_VARIANT_AUTO. */
+TB_API int tb_gpu_tiled_multiply_flat(int32_t device, const double* a, const double* b,
+                               int64_t m, int64_t k, int64_t n, int32_t tile_edge,
+                               double* out_c, int64_t out_c_len, double* out_seconds);
+
+/* Same as above with an explicit variant and an optional end-to-end clock:
+ * out_e2e_seconds (nullable) receives device time from the first H2D copy to
+ * the end of the D2H copy, on one stream (the `e2e` bench leg). */
+TB_API int tb_gpu_tiled_multiply_flat_ex(int32_t device, const double* a, const double* b,
+                                  int64_t m, int64_t k, int64_t n, int32_t tile_edge,
+                                  int32_t variant, double* out_c, int64_t out_c_len,
+                                  double* out_seconds, double* out_e2e_seconds);
+
+/* Device-pointer form used by the Python MultiplyFn backend (the "gpu-tiled"
+ * registration, registry.ts:58-71 / backends.py:270-272): synchronous,
+ * kernel-only seconds from events on `cuda_stream` (a cudaStream_t; NULL =
+ * legacy default stream). Square or rectangular, packed leading dims. */
+TB_API int tb_dgemm(const double* A, const double* B, double* C, int64_t m, int64_t k, int64_t n,
+             int32_t tile_edge, int32_t variant, int32_t device, void* cuda_stream,
+             double* out_kernel_seconds);
+
+/* Asynchronous launch with explicit leading dims and C += A·B when
+ * `accumulate` != 0 (the K-panel step of the row-sharded multi-GPU driver,
+ * SURVEY.md §8(e)). No synchronisation, no timing; errors from the launch
+ * itself are reported. Runs on the current device. */
+TB_API int tb_dgemm_launch(const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
+                    int64_t ldc, int64_t m, int64_t k, int64_t n, int32_t accumulate,
+                    int32_t tile_edge, int32_t variant, void* cuda_stream);
+
+/* cuBLAS DGEMM baseline (the paper's CuBLAS row; SPEC.md:15
+ * external registration) with the tb_dgemm signature; variant/tile ignored.
+ * Native FP64 (no emulation API exists for DGEMM in this toolkit). */
+TB_API int tb_cublas_dgemm(const double* A, const double* B, double* C, int64_t m, int64_t k,
+                    int64_t n, int32_t tile_edge, int32_t variant, int32_t device,
+                    void* cuda_stream, double* out_kernel_seconds);
+
+/* Launch validation only (limits.ts:58-79 validateLaunch), no device work
+ * beyond attribute queries: returns the status tb_dgemm would return for
+ * these arguments before launching. */
+TB_API int tb_validate_launch(int64_t m, int64_t k, int64_t n, int32_t tile_edge, int32_t variant,
+                       int32_t device);
+
+/* Number of CUDA devices (0 when there is no driver / device) —
+ * probeDevice() (executor.ts:158-162). */
+TB_API int tb_device_count(void);
+
+/* Variant name ("paper", "dmma_tma", ...) or NULL when out of range. */
+TB_API const char* tb_variant_name(int32_t variant);
+
+/* The variant AUTO resolves to for these arguments (-1 on bad args). */
+TB_API int tb_resolve_variant(const void* A, int64_t lda, const void* B, int64_t ldb, int32_t variant);
+
+/* Thread-local message for the last failing call on this thread. */
+TB_API const char* tb_last_error(void);
+
+/* Library version string. */
+TB_API const char* tb_version(void);
+
+/* Free the cached host-entry workspaces and cuBLAS handles. */
+TB_API void tb_release(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TBGPU_H_ */

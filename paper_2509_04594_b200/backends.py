@@ -1,0 +1,364 @@
+"""The GPU backends behind the reference's plug-in API.
+
+Mirrors the reference's selector and registration surface
+(/root/reference/pkg/src/tilebench/backends.py:56-272;
+/root/reference/pkg/gpu/src/registry.ts:14-71):
+
+* ``MultiplyFn = fn(a, b) -> matrix`` (backends.py:56) — ``gpu_tiled_multiply``;
+* ``BackendDescriptor`` / ``BackendRegistry`` / ``register_external`` with the
+  same duplicate/unknown-name semantics (backends.py:193-272);
+* ``register_gpu_backend`` adds "gpu-tiled" only when a CUDA device exists and
+  is a silent no-op otherwise (registry.ts:58-71);
+* ``register_into`` registers the same callables into the reference's own
+  ``tilebench`` registry (the drop-in path of demos/06_external_backends.py).
+
+Device buffers are torch CUDA tensors; arithmetic is the sm_100a kernels of
+``libtbgpu.so`` reached through the C ABI (``include/tbgpu.h``). There is no
+CPU path: without the library or a device these functions raise.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from typing import Callable
+
+import numpy as np
+
+from . import _lib
+from .errors import BackendConflictError, InvalidConfigError, ShapeError, UnknownBackendError
+from .matrices import require_operands
+
+__all__ = [
+    "MultiplyFn", "TileConfig", "BackendDescriptor", "BackendRegistry", "GPU_BACKEND_NAME",
+    "CUBLAS_BACKEND_NAME", "PAPER_BACKEND_NAME", "dgemm", "dgemm_launch", "cublas_dgemm",
+    "gpu_tiled_multiply", "gpu_tiled_multiply_timed", "gpu_tiled_multiply_flat", "cublas_multiply",
+    "cublas_multiply_timed", "default_registry", "register_external", "register_gpu_backend",
+    "register_into", "probe_device",
+]
+
+MultiplyFn = Callable[[np.ndarray, np.ndarray], np.ndarray]
+TimedMultiplyFn = Callable[[np.ndarray, np.ndarray], "tuple[np.ndarray, float]"]
+
+GPU_BACKEND_NAME = "gpu-tiled"  # registry.ts:50
+PAPER_BACKEND_NAME = "gpu-paper-k32"
+CUBLAS_BACKEND_NAME = "cublas-dgemm"
+
+
+@dataclass(frozen=True)
+class TileConfig:
+    """Tile edge K (default 32, limits.ts:40-42). The paper variant uses a
+    K x K thread block; the DMMA variants validate K like the reference
+    (K < 1 -> ShapeError, K*K > 1024 -> InvalidConfigError) and run their
+    fixed 128 x 128 x 16 CTA tile."""
+
+    k: int = _lib.DEFAULT_TILE_EDGE
+
+    def validate(self) -> None:
+        if self.k < 1:
+            raise InvalidConfigError(f"tile edge must be >= 1, got {self.k}")
+
+
+@dataclass(frozen=True)
+class BackendDescriptor:
+    name: str
+    parallel: bool = False
+    requires_external: bool = False
+
+
+# --------------------------------------------------------------------------
+# torch-tensor entry points (device pointers through the C ABI)
+# --------------------------------------------------------------------------
+
+def _torch():
+    import torch
+    return torch
+
+
+def _check_tensor(t, name: str, torch):
+    if not isinstance(t, torch.Tensor):
+        raise ShapeError(f"{name} must be a torch tensor")
+    if t.device.type != "cuda":
+        raise ShapeError(f"{name} must be a CUDA tensor, got {t.device}")
+    if t.dtype != torch.float64:
+        raise ShapeError(f"{name} must be float64, got {t.dtype}")
+    if t.dim() != 2:
+        raise ShapeError(f"{name} must be 2-D, got {t.dim()}-D")
+
+
+def _stream_handle(stream, torch) -> int:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return int(stream.cuda_stream)
+
+
+def dgemm(a, b, out=None, *, tile_edge: int = _lib.DEFAULT_TILE_EDGE, variant="auto", stream=None):
+    """C = A·B on CUDA float64 tensors (row-major, contiguous); synchronous.
+
+    Returns ``(out, kernel_seconds)`` — kernel-only CUDA-event time on the
+    launching stream (executor.ts:104,144)."""
+    torch = _torch()
+    _check_tensor(a, "a", torch)
+    _check_tensor(b, "b", torch)
+    if a.shape[1] != b.shape[0]:
+        raise ShapeError(f"inner dimensions differ: {a.shape[0]}x{a.shape[1]} @ {b.shape[0]}x{b.shape[1]}")
+    if a.device != b.device:
+        raise ShapeError(f"operands on different devices: {a.device} vs {b.device}")
+    a = a.contiguous()
+    b = b.contiguous()
+    m, k, n = a.shape[0], a.shape[1], b.shape[1]
+    if out is None:
+        out = torch.empty((m, n), dtype=torch.float64, device=a.device)
+    else:
+        _check_tensor(out, "out", torch)
+        if tuple(out.shape) != (m, n) or not out.is_contiguous() or out.device != a.device:
+            raise ShapeError(f"out must be a contiguous {m}x{n} tensor on {a.device}")
+    sec = ctypes.c_double(0.0)
+    st = _lib.lib().tb_dgemm(a.data_ptr(), b.data_ptr(), out.data_ptr(), m, k, n, int(tile_edge),
+                             _lib.variant_id(variant), a.device.index, _stream_handle(stream, torch),
+                             ctypes.byref(sec))
+    _lib.check(st)
+    return out, sec.value
+
+
+def dgemm_launch(a, b, out, *, accumulate: bool = False, tile_edge: int = _lib.DEFAULT_TILE_EDGE,
+                 variant="auto", stream=None) -> None:
+    """Asynchronous ``out (+)= a @ b`` on the current device and stream.
+
+    ``a``/``b``/``out`` may be row-slices or column-slices of larger row-major
+    tensors (unit inner stride; leading dim = stride(0)), which is how the
+    multi-GPU driver addresses K-panels without copies."""
+    torch = _torch()
+    for t, nm in ((a, "a"), (b, "b"), (out, "out")):
+        _check_tensor(t, nm, torch)
+        if t.stride(1) != 1:
+            raise ShapeError(f"{nm} must have unit column stride")
+    m, k, n = a.shape[0], a.shape[1], b.shape[1]
+    if b.shape[0] != k or tuple(out.shape) != (m, n):
+        raise ShapeError(f"shapes {tuple(a.shape)} @ {tuple(b.shape)} -> {tuple(out.shape)} do not chain")
+    st = _lib.lib().tb_dgemm_launch(a.data_ptr(), a.stride(0), b.data_ptr(), b.stride(0), out.data_ptr(),
+                                    out.stride(0), m, k, n, 1 if accumulate else 0, int(tile_edge),
+                                    _lib.variant_id(variant), _stream_handle(stream, torch))
+    _lib.check(st)
+
+
+def cublas_dgemm(a, b, out=None, *, stream=None):
+    """cuBLAS DGEMM baseline (the paper's CuBLAS row) with ``dgemm``'s contract."""
+    torch = _torch()
+    _check_tensor(a, "a", torch)
+    _check_tensor(b, "b", torch)
+    a = a.contiguous()
+    b = b.contiguous()
+    m, k, n = a.shape[0], a.shape[1], b.shape[1]
+    if b.shape[0] != k:
+        raise ShapeError(f"inner dimensions differ: {m}x{k} @ {b.shape[0]}x{n}")
+    if out is None:
+        out = torch.empty((m, n), dtype=torch.float64, device=a.device)
+    sec = ctypes.c_double(0.0)
+    st = _lib.lib().tb_cublas_dgemm(a.data_ptr(), b.data_ptr(), out.data_ptr(), m, k, n, 32, 0,
+                                    a.device.index, _stream_handle(stream, torch), ctypes.byref(sec))
+    _lib.check(st)
+    return out, sec.value
+
+
+# --------------------------------------------------------------------------
+# numpy MultiplyFn entry points (the harness's fn(a, b) -> matrix)
+# --------------------------------------------------------------------------
+
+def _device_index(device) -> int:
+    return 0 if device is None else int(device)
+
+
+def gpu_tiled_multiply_timed(a, b, tile: TileConfig = TileConfig(), variant="auto", device=None):
+    """``(product, kernel_seconds)``: upload, sm_100a kernel, download.
+
+    Uploads/downloads sit outside the kernel clock, exactly as the reference
+    device copies operands before its clock starts (executor.ts:92-104)."""
+    torch = _torch()
+    a, b = require_operands(a, b)
+    tile.validate()
+    dev = torch.device("cuda", _device_index(device))
+    ta = torch.from_numpy(a).to(dev)
+    tb = torch.from_numpy(b).to(dev)
+    out, sec = dgemm(ta, tb, tile_edge=tile.k, variant=variant)
+    return out.cpu().numpy(), sec
+
+
+def gpu_tiled_multiply(a, b, tile: TileConfig = TileConfig(), variant="auto", device=None) -> np.ndarray:
+    """``MultiplyFn`` form (backends.py:56): fresh product, inputs untouched."""
+    return gpu_tiled_multiply_timed(a, b, tile, variant, device)[0]
+
+
+def cublas_multiply_timed(a, b, device=None):
+    torch = _torch()
+    a, b = require_operands(a, b)
+    dev = torch.device("cuda", _device_index(device))
+    out, sec = cublas_dgemm(torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev))
+    return out.cpu().numpy(), sec
+
+
+def cublas_multiply(a, b, device=None) -> np.ndarray:
+    return cublas_multiply_timed(a, b, device)[0]
+
+
+def gpu_tiled_multiply_flat(device, a, b, m, k, n, tile_edge, out_c, out_seconds, variant="auto",
+                            out_e2e_seconds=None) -> int:
+    """gpuTiledMultiplyFlat (multiply.ts:54-79) over host buffers: numpy
+    arrays (or pinned torch CPU tensors) in, status code out; ``out_c`` and
+    ``out_seconds`` are caller-owned out-parameters. ``device=None`` ->
+    STATUS_NO_DEVICE, as for a null device in the reference."""
+
+    def ptr(x):
+        if x is None:
+            return None
+        if hasattr(x, "data_ptr"):
+            return x.data_ptr()
+        return x.ctypes.data
+
+    def length(x):
+        return x.numel() if hasattr(x, "numel") else x.size
+
+    if device is None:
+        return _lib.STATUS_NO_DEVICE
+    for x in (a, b, out_c):
+        if hasattr(x, "dtype") and str(x.dtype) not in ("float64", "torch.float64"):
+            return _lib.STATUS_BAD_DIMS
+    if length(out_seconds) < 1:
+        return _lib.STATUS_BAD_DIMS
+    sec = ctypes.c_double(0.0)
+    e2e = ctypes.c_double(0.0)
+    st = _lib.lib().tb_gpu_tiled_multiply_flat_ex(int(device), ptr(a), ptr(b), int(m), int(k), int(n),
+                                                  int(tile_edge), _lib.variant_id(variant), ptr(out_c),
+                                                  int(length(out_c)), ctypes.byref(sec), ctypes.byref(e2e))
+    if st == _lib.STATUS_OK:
+        out_seconds[0] = sec.value
+        if out_e2e_seconds is not None:
+            out_e2e_seconds[0] = e2e.value
+    return st
+
+
+# --------------------------------------------------------------------------
+# registry (backends.py:193-272 semantics)
+# --------------------------------------------------------------------------
+
+def probe_device() -> int | None:
+    """First CUDA device index, or None (executor.ts:158-162 probeDevice)."""
+    try:
+        return 0 if _lib.device_count() > 0 else None
+    except OSError:
+        return None
+
+
+class BackendRegistry:
+    """Name-based lookup of multiplication backends (backends.py:193-237).
+
+    Entries hold a ``build(tile, pool) -> MultiplyFn`` and, for the GPU
+    backends, a kernel-timed sibling used by the device-timed harness."""
+
+    def __init__(self, include_builtins: bool = True, device=None):
+        self._entries: dict[str, tuple[BackendDescriptor, Callable, Callable | None]] = {}
+        if include_builtins:
+            register_gpu_backend(self, device=device)
+
+    def _register(self, descriptor, build, timed_build=None) -> BackendDescriptor:
+        if descriptor.name in self._entries:
+            raise BackendConflictError(f"backend {descriptor.name!r} is already registered")
+        self._entries[descriptor.name] = (descriptor, build, timed_build)
+        return descriptor
+
+    def register_external(self, descriptor: BackendDescriptor, fn: MultiplyFn, timed_fn=None) -> BackendDescriptor:
+        """Register a ready-made fn(a, b) under a unique name (backends.py:213-215)."""
+        return self._register(descriptor, lambda tile, pool: fn,
+                              (lambda tile, pool: timed_fn) if timed_fn is not None else None)
+
+    def unregister(self, name: str) -> None:
+        self._entries.pop(name, None)
+
+    def names(self) -> list[str]:
+        return list(self._entries)
+
+    def descriptor(self, name: str) -> BackendDescriptor:
+        try:
+            return self._entries[name][0]
+        except KeyError:
+            raise UnknownBackendError(self._unknown_message(name)) from None
+
+    def resolve(self, name: str, tile: TileConfig = TileConfig(), pool=None) -> MultiplyFn:
+        try:
+            _, build, _ = self._entries[name]
+        except KeyError:
+            raise UnknownBackendError(self._unknown_message(name)) from None
+        return build(tile, pool)
+
+    def resolve_timed(self, name: str, tile: TileConfig = TileConfig(), pool=None):
+        """``fn(a, b) -> (product, kernel_seconds)``, or None for backends
+        without a device clock (the harness then wall-clocks them)."""
+        try:
+            _, _, timed = self._entries[name]
+        except KeyError:
+            raise UnknownBackendError(self._unknown_message(name)) from None
+        return timed(tile, pool) if timed is not None else None
+
+    def _unknown_message(self, name: str) -> str:
+        return f"unknown backend {name!r}; registered: {', '.join(self._entries)}"
+
+
+def register_gpu_backend(registry: BackendRegistry | None = None, device=None, variant="auto"):
+    """Register "gpu-tiled", "gpu-paper-k32" and "cublas-dgemm" when a CUDA
+    device exists; silent no-op (returns None) otherwise (registry.ts:58-71)."""
+    registry = registry if registry is not None else default_registry()
+    if device is None:
+        device = probe_device()
+    if device is None:
+        return None
+    desc = registry._register(
+        BackendDescriptor(GPU_BACKEND_NAME, parallel=True, requires_external=True),
+        lambda tile, pool: (lambda a, b: gpu_tiled_multiply(a, b, tile, variant, device)),
+        lambda tile, pool: (lambda a, b: gpu_tiled_multiply_timed(a, b, tile, variant, device)),
+    )
+    registry._register(
+        BackendDescriptor(PAPER_BACKEND_NAME, parallel=True, requires_external=True),
+        lambda tile, pool: (lambda a, b: gpu_tiled_multiply(a, b, tile, "paper", device)),
+        lambda tile, pool: (lambda a, b: gpu_tiled_multiply_timed(a, b, tile, "paper", device)),
+    )
+    registry._register(
+        BackendDescriptor(CUBLAS_BACKEND_NAME, parallel=True, requires_external=True),
+        lambda tile, pool: (lambda a, b: cublas_multiply(a, b, device)),
+        lambda tile, pool: (lambda a, b: cublas_multiply_timed(a, b, device)),
+    )
+    return desc
+
+
+def register_into(tilebench_registry, descriptor_cls, device=None, variant="auto"):
+    """Drop-in: register the GPU MultiplyFns into the REFERENCE's registry
+    (``tilebench.BackendRegistry.register_external``, backends.py:213-215),
+    using its own ``BackendDescriptor`` class. No-op without a device."""
+    if device is None:
+        device = probe_device()
+    if device is None:
+        return []
+    tile = TileConfig()
+    out = [
+        tilebench_registry.register_external(
+            descriptor_cls(GPU_BACKEND_NAME, parallel=True, requires_external=True),
+            lambda a, b: gpu_tiled_multiply(a, b, tile, variant, device)),
+        tilebench_registry.register_external(
+            descriptor_cls(CUBLAS_BACKEND_NAME, parallel=True, requires_external=True),
+            lambda a, b: cublas_multiply(a, b, device)),
+    ]
+    return out
+
+
+_default_registry: BackendRegistry | None = None
+
+
+def default_registry() -> BackendRegistry:
+    """Process-wide registry: the GPU built-ins (when a device exists) plus external additions."""
+    global _default_registry
+    if _default_registry is None:
+        _default_registry = BackendRegistry()
+    return _default_registry
+
+
+def register_external(descriptor: BackendDescriptor, fn: MultiplyFn) -> BackendDescriptor:
+    """Register an external backend on the default registry (backends.py:270-272)."""
+    return default_registry().register_external(descriptor, fn)

@@ -1,0 +1,247 @@
+// dgemm_dmma.cuh — sm_100a FP64 GEMM on the DMMA pipe (mma.sync m8n8k4 f64).
+//
+// The paper's K = 32 tiled kernel (reference kernel.ts:50-78)
+// "revisited for Blackwell": instead of one output per thread fed by two
+// shared-memory loads per FMA, a 128 x 128 CTA tile is computed by 8 consumer
+// warps (64 x 32 warp tiles, 32 DMMA accumulators each) while a producer warp
+// streams 128 x 16 / 16 x 128 k-slabs of A and B into a STAGES-deep
+// shared-memory ring (TMA with SWIZZLE_128B, or 8-byte cp.async with zero fill
+// when the TMA 16-byte alignment rule does not hold). Full/empty mbarriers hand
+// stages between producer and consumers; there is no __syncthreads in the main
+// loop.
+//
+// Bank-conflict-free fragment loads. With the swizzled layout, the natural
+// DMMA k order (lane q feeds k = 4s + q) gives 2-way conflicts. The k index
+// inside a 16-deep slab is therefore permuted (legal: it only reorders the
+// sum): lane q feeds k-pair PA(q) = {0,2,5,7}[q] to DMMA steps 0 and 1 and
+// PB(q) = PA(q) ^ 1 = {1,3,4,6}[q] to steps 2 and 3. A fragments then come in
+// as one conflict-free 128-bit load per two steps, B fragments as
+// conflict-free 64-bit loads (derivation in DESIGN.md §4).
+#pragma once
+#include <cstdint>
+#include <cuda.h>
+#include "ptx.cuh"
+
+namespace tb {
+
+enum class Loader : int { TMA = 0, CPASYNC = 1 };
+
+struct DmmaCfg {
+  static constexpr int BM = 128, BN = 128, BK = 16;
+  static constexpr int WARPS_M = 2, WARPS_N = 4;
+  static constexpr int WM = BM / WARPS_M;  // 64
+  static constexpr int WN = BN / WARPS_N;  // 32
+  static constexpr int MI = WM / 8;        // 8 DMMA rows per warp
+  static constexpr int NI = WN / 8;        // 4 DMMA cols per warp
+  static constexpr int CONSUMER_WARPS = WARPS_M * WARPS_N;
+  // Warpgroup specialisation: warpgroup 0 = producer (one TMA-issuing lane, or
+  // all 4 warps issuing cp.async), warpgroups 1-2 = the 8 consumer warps.
+  // setmaxnreg moves registers from the producer to the consumers
+  // (4*32*PRODUCER_REGS + 8*32*CONSUMER_REGS <= 64K).
+  static constexpr int THREADS = (CONSUMER_WARPS + 4) * 32;
+  static constexpr int PRODUCER_REGS = 40;
+  static constexpr int CONSUMER_REGS = 232;
+  static constexpr int A_STAGE = BM * BK * 8;  // 16 KB: [128 rows][16 k] swizzled
+  static constexpr int B_STAGE = BK * BN * 8;  // 16 KB: 8 boxes of [16 k][16 n] swizzled
+  static constexpr int STAGE = A_STAGE + B_STAGE;
+  static constexpr int B_BOX = BK * 16 * 8;  // 2 KB
+  static constexpr int GROUP_M = 8;          // tile raster: GROUP_M tile-rows per band
+};
+
+template <int STAGES>
+constexpr int dmma_smem_bytes() {
+  return STAGES * DmmaCfg::STAGE + 2 * STAGES * 8 + 1024;  // + barriers + alignment slack
+}
+
+struct GemmParams {
+  const double* A;
+  const double* B;
+  double* C;
+  int64_t lda, ldb, ldc;
+  int m, n, k;
+  int tiles_m, tiles_n;
+  int accumulate;  // C += A·B instead of C = A·B
+  int vec_store;   // C rows 16-byte aligned: store double2
+};
+
+// Grouped raster over the (tile_m, tile_n) grid so concurrently resident CTAs
+// share A row-panels and B column-panels in L2.
+__device__ __forceinline__ void tile_coords(int tile, int tiles_m, int tiles_n, int& tm, int& tn) {
+  const int group = DmmaCfg::GROUP_M * tiles_n;
+  const int first_m = (tile / group) * DmmaCfg::GROUP_M;
+  const int gm = min(tiles_m - first_m, DmmaCfg::GROUP_M);
+  const int r = tile % group;
+  tm = first_m + r % gm;
+  tn = r / gm;
+}
+
+template <int STAGES, Loader LD>
+__global__ void __launch_bounds__(DmmaCfg::THREADS, 1)
+    dgemm_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                      const GemmParams p) {
+  using C = DmmaCfg;
+  extern __shared__ uint8_t smem_raw[];
+  // SWIZZLE_128B's XOR pattern is a function of absolute smem address bits
+  // [4:6] ^ [7:9]: stage buffers must start on 1024-byte boundaries.
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE);
+  uint64_t* empty = full + STAGES;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int tm, tn;
+  tile_coords(blockIdx.x, p.tiles_m, p.tiles_n, tm, tn);
+  const int m0 = tm * C::BM, n0 = tn * C::BN;
+  const int num_k = (p.k + C::BK - 1) / C::BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(smem_u32(&full[s]), LD == Loader::TMA ? 1 : 128);
+      mbar_init(smem_u32(&empty[s]), C::CONSUMER_WARPS);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+
+  if (warp < 4) {
+    // ------------------------------------------------------------ producer
+    setmaxnreg_dec<C::PRODUCER_REGS>();
+    if constexpr (LD == Loader::TMA) {
+      if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&tmA);
+        tma_prefetch_desc(&tmB);
+        for (int kt = 0; kt < num_k; ++kt) {
+          const int s = kt % STAGES;
+          const uint32_t ph = (kt / STAGES) & 1;
+          if (kt >= STAGES) mbar_wait(smem_u32(&empty[s]), ph ^ 1);
+          const uint32_t fb = smem_u32(&full[s]);
+          const uint32_t sa = smem_u32(smem + s * C::STAGE);
+          const uint32_t sb = sa + C::A_STAGE;
+          mbar_arrive_expect_tx(fb, C::STAGE);  // OOB-filled boxes still count full bytes
+          tma_load_2d(sa, &tmA, fb, kt * C::BK, m0);
+#pragma unroll
+          for (int j = 0; j < C::BN / 16; ++j) tma_load_2d(sb + j * C::B_BOX, &tmB, fb, n0 + 16 * j, kt * C::BK);
+        }
+      }
+    } else {
+      // 8-byte cp.async into the same swizzled layout; src-size 0 zero-fills
+      // out-of-range cells (the paper's "load zero" edge rule).
+      for (int kt = 0; kt < num_k; ++kt) {
+        const int s = kt % STAGES;
+        const uint32_t ph = (kt / STAGES) & 1;
+        if (kt >= STAGES) mbar_wait(smem_u32(&empty[s]), ph ^ 1);
+        const uint32_t sa = smem_u32(smem + s * C::STAGE);
+        const uint32_t sb = sa + C::A_STAGE;
+        const int k0 = kt * C::BK;
+        const int pt = threadIdx.x;  // 0..127
+#pragma unroll 4
+        for (int it = 0; it < (C::BM * C::BK) / 128; ++it) {
+          const int e = it * 128 + pt, r = e >> 4, kk = e & 15;
+          const int gm = m0 + r, gk = k0 + kk;
+          const bool ok = gm < p.m && gk < p.k;
+          const double* src = ok ? p.A + (int64_t)gm * p.lda + gk : p.A;
+          cp_async_8(sa + r * 128 + (((kk >> 1) ^ (r & 7)) << 4) + (kk & 1) * 8, src, ok);
+        }
+#pragma unroll 4
+        for (int it = 0; it < (C::BK * C::BN) / 128; ++it) {
+          const int e = it * 128 + pt, kr = e >> 7, nn = e & 127;
+          const int gk = k0 + kr, gn = n0 + nn;
+          const bool ok = gk < p.k && gn < p.n;
+          const double* src = ok ? p.B + (int64_t)gk * p.ldb + gn : p.B;
+          cp_async_8(sb + (nn >> 4) * C::B_BOX + kr * 128 + ((((nn & 15) >> 1) ^ (kr & 7)) << 4) + (nn & 1) * 8,
+                     src, ok);
+        }
+        cp_async_mbar_arrive_noinc(smem_u32(&full[s]));
+      }
+    }
+    return;
+  }
+
+  // -------------------------------------------------------------- consumers
+  setmaxnreg_inc<C::CONSUMER_REGS>();
+  const int cw = warp - 4;
+  const int wm = cw / C::WARPS_N, wn = cw % C::WARPS_N;
+  const int q = lane & 3, g = lane >> 2;
+  const int pa = 2 * q + (q >> 1);  // {0,2,5,7}
+  const int pb = pa ^ 1;            // {1,3,4,6}
+
+  // A: row r = wm*64 + mi*8 + g (so r & 7 == g), 16-byte chunk c -> c ^ g.
+  const uint32_t a_off0 = (wm * C::WM + g) * 128 + ((pa ^ g) << 4);
+  const uint32_t a_off1 = (wm * C::WM + g) * 128 + ((pb ^ g) << 4);
+  // B: column nn = (ni&1)*8 + g inside box wn*2 + (ni>>1); k row kv:
+  // byte = box*2048 + kv*128 + (((nn>>1) ^ (kv&7)) << 4) + (nn&1)*8, and
+  // (ni&1) flips chunk bit 2, i.e. byte bit 6.
+  uint32_t b_off[4];
+  {
+    const int kv[4] = {2 * pa, 2 * pa + 1, 2 * pb, 2 * pb + 1};
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      b_off[e] = wn * 2 * C::B_BOX + kv[e] * 128 + ((((g >> 1) ^ (kv[e] & 7))) << 4) + (g & 1) * 8;
+  }
+
+  double acc[C::MI][C::NI][2];
+#pragma unroll
+  for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+    for (int j = 0; j < C::NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  for (int kt = 0; kt < num_k; ++kt) {
+    const int s = kt % STAGES;
+    const uint32_t ph = (kt / STAGES) & 1;
+    mbar_wait(smem_u32(&full[s]), ph);
+    const uint8_t* sa = smem + s * C::STAGE;
+    const uint8_t* sb = sa + C::A_STAGE;
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      double2 af[C::MI];
+      double bf[2][C::NI];
+#pragma unroll
+      for (int i = 0; i < C::MI; ++i)
+        af[i] = *reinterpret_cast<const double2*>(sa + (half ? a_off1 : a_off0) + i * 8 * 128);
+#pragma unroll
+      for (int j = 0; j < C::NI; ++j) {
+        const uint32_t box = (j >> 1) * C::B_BOX, flip = (j & 1) ? 64u : 0u;
+        bf[0][j] = *reinterpret_cast<const double*>(sb + box + (b_off[2 * half] ^ flip));
+        bf[1][j] = *reinterpret_cast<const double*>(sb + box + (b_off[2 * half + 1] ^ flip));
+      }
+#pragma unroll
+      for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+        for (int j = 0; j < C::NI; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i].x, bf[0][j]);
+#pragma unroll
+      for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+        for (int j = 0; j < C::NI; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i].y, bf[1][j]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(smem_u32(&empty[s]));
+  }
+
+  // --------------------------------------------------------------- epilogue
+#pragma unroll
+  for (int i = 0; i < C::MI; ++i) {
+    const int r = m0 + wm * C::WM + i * 8 + g;
+    if (r >= p.m) continue;
+    double* crow = p.C + (int64_t)r * p.ldc;
+#pragma unroll
+    for (int j = 0; j < C::NI; ++j) {
+      const int c = n0 + wn * C::WN + j * 8 + 2 * q;
+      double v0 = acc[i][j][0], v1 = acc[i][j][1];
+      if (c + 1 < p.n) {
+        if (p.accumulate) {
+          v0 += crow[c];
+          v1 += crow[c + 1];
+        }
+        if (p.vec_store) {
+          *reinterpret_cast<double2*>(crow + c) = make_double2(v0, v1);
+        } else {
+          crow[c] = v0;
+          crow[c + 1] = v1;
+        }
+      } else if (c < p.n) {
+        crow[c] = p.accumulate ? v0 + crow[c] : v0;
+      }
+    }
+  }
+}
+
+}  // namespace tb

@@ -1,0 +1,488 @@
+// tb_capi.cu — the extern "C" boundary (include/tbgpu.h): launch validation
+// with the reference's status codes, variant dispatch, TMA descriptor
+// encoding, kernel-only CUDA-event timing, the host-buffer flat entry and the
+// cuBLAS DGEMM baseline.
+#include <cublas_v2.h>
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "../../include/tbgpu.h"
+#include "dgemm_dmma.cuh"
+#include "dgemm_paper.cuh"
+
+#ifndef TB_VERSION
+#define TB_VERSION "tbgpu 0.1.0 (sm_100a)"
+#endif
+
+namespace {
+
+constexpr int kStages = 6;                 // 6 x 32 KB ring = 192 KB of the 227 KB opt-in
+constexpr int kMaxDevices = 64;
+constexpr int kMaxBlockThreads = 1024;     // limits.ts:20-24 maxThreadsPerBlock
+
+thread_local char g_err[512] = "";
+
+void set_err(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  set_err("%s: %s", what, cudaGetErrorString(e));
+  return TB_STATUS_RUNTIME;
+}
+
+#define TB_CUDA(call, what)                          \
+  do {                                               \
+    cudaError_t e_ = (call);                         \
+    if (e_ != cudaSuccess) return cuda_fail(e_, what); \
+  } while (0)
+
+struct DeviceState {
+  std::mutex mu;       // device attributes, kernel attributes, cuBLAS handle
+  std::mutex host_mu;  // host-buffer entry: workspace + stream
+  bool ready = false;
+  int sms = 0;
+  int smem_optin = 0;
+  bool attrs_set = false;
+  cublasHandle_t cublas = nullptr;
+  cudaStream_t host_stream = nullptr;  // stream of the host-buffer entry
+  double* ws = nullptr;                // host-entry device workspace (A | B | C)
+  size_t ws_bytes = 0;
+};
+
+DeviceState g_dev[kMaxDevices];
+
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+std::once_flag g_encode_once;
+
+int device_count_raw() {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+// RAII: switch to `dev` for the call, restore the caller's device after.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+int ensure_device(int dev) {
+  DeviceState& st = g_dev[dev];
+  std::lock_guard<std::mutex> lk(st.mu);
+  if (st.ready) return TB_STATUS_OK;
+  TB_CUDA(cudaDeviceGetAttribute(&st.sms, cudaDevAttrMultiProcessorCount, dev), "query SM count");
+  TB_CUDA(cudaDeviceGetAttribute(&st.smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev),
+          "query shared memory opt-in");
+  st.ready = true;
+  return TB_STATUS_OK;
+}
+
+int ensure_kernel_attrs(int dev) {
+  DeviceState& st = g_dev[dev];
+  std::lock_guard<std::mutex> lk(st.mu);
+  if (st.attrs_set) return TB_STATUS_OK;
+  const int bytes = tb::dmma_smem_bytes<kStages>();
+  TB_CUDA(cudaFuncSetAttribute(tb::dgemm_dmma_kernel<kStages, tb::Loader::TMA>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
+          "set smem attribute (dmma_tma)");
+  TB_CUDA(cudaFuncSetAttribute(tb::dgemm_dmma_kernel<kStages, tb::Loader::CPASYNC>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
+          "set smem attribute (dmma_cpasync)");
+  TB_CUDA(cudaFuncSetAttribute(tb::dgemm_paper_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               st.smem_optin),
+          "set smem attribute (paper)");
+  st.attrs_set = true;
+  return TB_STATUS_OK;
+}
+
+int get_encoder() {
+  std::call_once(g_encode_once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    else
+      cudaGetLastError();
+  });
+  if (!g_encode) {
+    set_err("cuTensorMapEncodeTiled unavailable from the driver");
+    return TB_STATUS_RUNTIME;
+  }
+  return TB_STATUS_OK;
+}
+
+// Row-major [rows][cols] float64 with leading dim ld, box [box_rows][16 cols], SWIZZLE_128B.
+int encode_map(CUtensorMap* map, const double* base, int64_t rows, int64_t cols, int64_t ld, uint32_t box_rows) {
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(double)};
+  cuuint32_t box[2] = {16u, box_rows};
+  cuuint32_t estr[2] = {1u, 1u};
+  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box,
+                        estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_err("cuTensorMapEncodeTiled failed (CUresult %d) for %lldx%lld ld=%lld", (int)r, (long long)rows,
+            (long long)cols, (long long)ld);
+    return TB_STATUS_RUNTIME;
+  }
+  return TB_STATUS_OK;
+}
+
+bool tma_ok(const void* A, int64_t lda, const void* B, int64_t ldb) {
+  // TMA: 16-byte aligned global base and 16-byte multiple strides (cuda.h
+  // cuTensorMapEncodeTiled requirements), i.e. even leading dims for float64.
+  return ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15u) == 0 && (lda % 2 == 0) &&
+         (ldb % 2 == 0);
+}
+
+int resolve(const void* A, int64_t lda, const void* B, int64_t ldb, int variant) {
+  if (variant == TB_VARIANT_AUTO) return tma_ok(A, lda, B, ldb) ? TB_VARIANT_DMMA_TMA : TB_VARIANT_DMMA_CPASYNC;
+  if (variant == TB_VARIANT_DMMA_TMA && !tma_ok(A, lda, B, ldb)) return TB_VARIANT_DMMA_CPASYNC;
+  return variant;
+}
+
+// validateLaunch (limits.ts:58-79) plus this kernel family's own limits.
+int validate(int64_t m, int64_t k, int64_t n, int32_t tile_edge, int32_t variant, int dev) {
+  if (m < 1 || k < 1 || n < 1) {
+    set_err("dimensions must be positive integers, got %lldx%lld @ %lldx%lld", (long long)m, (long long)k,
+            (long long)k, (long long)n);
+    return TB_STATUS_BAD_DIMS;
+  }
+  if (variant < 0 || variant >= TB_NUM_VARIANTS) {
+    set_err("unknown kernel variant %d", variant);
+    return TB_STATUS_BAD_DIMS;
+  }
+  if (tile_edge < 1) {
+    set_err("tile edge must be a positive integer, got %d", tile_edge);
+    return TB_STATUS_BAD_DIMS;
+  }
+  const int64_t threads = (int64_t)tile_edge * tile_edge;
+  if (threads > kMaxBlockThreads) {
+    set_err("block of %lld threads (%dx%d) exceeds the device limit of %d threads per block", (long long)threads,
+            tile_edge, tile_edge, kMaxBlockThreads);
+    return TB_STATUS_OVER_LIMITS;
+  }
+  const int64_t lim = 0x7fffffff;
+  if (m > lim || k > lim || n > lim) {
+    set_err("dimension over the 2^31-1 element limit of this kernel family");
+    return TB_STATUS_OVER_LIMITS;
+  }
+  if (dev >= 0) {
+    const DeviceState& st = g_dev[dev];
+    const int64_t shared = 2 * threads * (int64_t)sizeof(double);  // limits.ts:45-47
+    if (variant == TB_VARIANT_PAPER) {
+      if (shared > st.smem_optin) {
+        set_err("shared tiles need %lld bytes, over the per-block limit of %d bytes", (long long)shared,
+                st.smem_optin);
+        return TB_STATUS_OVER_LIMITS;
+      }
+      if ((m + tile_edge - 1) / tile_edge > 65535) {
+        set_err("grid of %lld tile rows exceeds gridDim.y 65535", (long long)((m + tile_edge - 1) / tile_edge));
+        return TB_STATUS_OVER_LIMITS;
+      }
+    } else if (tb::dmma_smem_bytes<kStages>() > st.smem_optin) {
+      set_err("dmma pipeline needs %d bytes of shared memory, device allows %d", tb::dmma_smem_bytes<kStages>(),
+              st.smem_optin);
+      return TB_STATUS_OVER_LIMITS;
+    }
+  }
+  return TB_STATUS_OK;
+}
+
+int check_device(int32_t device) {
+  const int count = device_count_raw();
+  if (count <= 0 || device < 0 || device >= count || device >= kMaxDevices) {
+    set_err("no CUDA device %d (found %d)", device, count);
+    return TB_STATUS_NO_DEVICE;
+  }
+  return ensure_device(device);
+}
+
+// Enqueue one GEMM on `stream` (current device = dev). Assumes validated args.
+int launch(int dev, const double* A, int64_t lda, const double* B, int64_t ldb, double* Cm, int64_t ldc, int64_t m,
+           int64_t k, int64_t n, int accumulate, int tile_edge, int variant, cudaStream_t stream) {
+  int s = ensure_kernel_attrs(dev);
+  if (s) return s;
+  variant = resolve(A, lda, B, ldb, variant);
+  if (variant == TB_VARIANT_PAPER) {
+    const int K = tile_edge;
+    dim3 block(K, K);
+    dim3 grid((unsigned)((n + K - 1) / K), (unsigned)((m + K - 1) / K));
+    tb::dgemm_paper_kernel<<<grid, block, 2 * K * K * sizeof(double), stream>>>(
+        A, lda, B, ldb, Cm, ldc, (int)m, (int)k, (int)n, K, accumulate);
+  } else {
+    using Cfg = tb::DmmaCfg;
+    tb::GemmParams p;
+    p.A = A;
+    p.B = B;
+    p.C = Cm;
+    p.lda = lda;
+    p.ldb = ldb;
+    p.ldc = ldc;
+    p.m = (int)m;
+    p.n = (int)n;
+    p.k = (int)k;
+    p.tiles_m = (int)((m + Cfg::BM - 1) / Cfg::BM);
+    p.tiles_n = (int)((n + Cfg::BN - 1) / Cfg::BN);
+    p.accumulate = accumulate;
+    p.vec_store = ((reinterpret_cast<uintptr_t>(Cm) & 15u) == 0 && ldc % 2 == 0) ? 1 : 0;
+    const int64_t tiles = (int64_t)p.tiles_m * p.tiles_n;
+    if (tiles > 0x7fffffff) {
+      set_err("too many output tiles");
+      return TB_STATUS_OVER_LIMITS;
+    }
+    CUtensorMap mA, mB;
+    std::memset(&mA, 0, sizeof(mA));
+    std::memset(&mB, 0, sizeof(mB));
+    const int bytes = tb::dmma_smem_bytes<kStages>();
+    if (variant == TB_VARIANT_DMMA_TMA) {
+      if ((s = get_encoder())) return s;
+      if ((s = encode_map(&mA, A, m, k, lda, Cfg::BM))) return s;
+      if ((s = encode_map(&mB, B, k, n, ldb, Cfg::BK))) return s;
+      tb::dgemm_dmma_kernel<kStages, tb::Loader::TMA><<<(unsigned)tiles, Cfg::THREADS, bytes, stream>>>(mA, mB, p);
+    } else {
+      tb::dgemm_dmma_kernel<kStages, tb::Loader::CPASYNC>
+          <<<(unsigned)tiles, Cfg::THREADS, bytes, stream>>>(mA, mB, p);
+    }
+  }
+  TB_CUDA(cudaGetLastError(), "kernel launch");
+  return TB_STATUS_OK;
+}
+
+struct EventPair {
+  cudaEvent_t a = nullptr, b = nullptr;
+  ~EventPair() {
+    if (a) cudaEventDestroy(a);
+    if (b) cudaEventDestroy(b);
+  }
+  int create() {
+    TB_CUDA(cudaEventCreate(&a), "event create");
+    TB_CUDA(cudaEventCreate(&b), "event create");
+    return TB_STATUS_OK;
+  }
+};
+
+int timed_gemm(int dev, const double* A, const double* B, double* Cm, int64_t m, int64_t k, int64_t n,
+               int tile_edge, int variant, cudaStream_t stream, double* out_seconds, bool use_cublas) {
+  EventPair ev;
+  int s = ev.create();
+  if (s) return s;
+  TB_CUDA(cudaEventRecord(ev.a, stream), "event record");
+  if (use_cublas) {
+    DeviceState& st = g_dev[dev];
+    {
+      std::lock_guard<std::mutex> lk(st.mu);
+      if (!st.cublas && cublasCreate(&st.cublas) != CUBLAS_STATUS_SUCCESS) {
+        set_err("cublasCreate failed");
+        return TB_STATUS_RUNTIME;
+      }
+    }
+    cublasSetStream(st.cublas, stream);
+    const double one = 1.0, zero = 0.0;
+    // Row-major C = A·B  <=>  column-major C^T = B^T · A^T.
+    if (cublasDgemm(st.cublas, CUBLAS_OP_N, CUBLAS_OP_N, (int)n, (int)m, (int)k, &one, B, (int)n, A, (int)k, &zero,
+                    Cm, (int)n) != CUBLAS_STATUS_SUCCESS) {
+      set_err("cublasDgemm failed");
+      return TB_STATUS_RUNTIME;
+    }
+  } else {
+    s = launch(dev, A, k, B, n, Cm, n, m, k, n, 0, tile_edge, variant, stream);
+    if (s) return s;
+  }
+  TB_CUDA(cudaEventRecord(ev.b, stream), "event record");
+  TB_CUDA(cudaEventSynchronize(ev.b), "kernel execution");
+  float ms = 0.f;
+  TB_CUDA(cudaEventElapsedTime(&ms, ev.a, ev.b), "event elapsed");
+  if (out_seconds) *out_seconds = (double)ms * 1e-3;
+  return TB_STATUS_OK;
+}
+
+int dgemm_common(const double* A, const double* B, double* Cm, int64_t m, int64_t k, int64_t n, int32_t tile_edge,
+                 int32_t variant, int32_t device, void* cuda_stream, double* out_seconds, bool use_cublas) {
+  int s = check_device(device);
+  if (s) return s;
+  if (!A || !B || !Cm || !out_seconds) {
+    set_err("null buffer pointer");
+    return TB_STATUS_BAD_DIMS;
+  }
+  if ((s = validate(m, k, n, tile_edge, variant, device))) return s;
+  DeviceGuard guard(device);
+  return timed_gemm(device, A, B, Cm, m, k, n, tile_edge, variant, static_cast<cudaStream_t>(cuda_stream),
+                    out_seconds, use_cublas);
+}
+
+}  // namespace
+
+extern "C" {
+
+int tb_device_count(void) { return device_count_raw(); }
+
+const char* tb_last_error(void) { return g_err; }
+
+const char* tb_version(void) { return TB_VERSION; }
+
+const char* tb_variant_name(int32_t variant) {
+  switch (variant) {
+    case TB_VARIANT_AUTO: return "auto";
+    case TB_VARIANT_PAPER: return "paper";
+    case TB_VARIANT_DMMA_TMA: return "dmma_tma";
+    case TB_VARIANT_DMMA_CPASYNC: return "dmma_cpasync";
+    default: return nullptr;
+  }
+}
+
+int tb_resolve_variant(const void* A, int64_t lda, const void* B, int64_t ldb, int32_t variant) {
+  if (variant < 0 || variant >= TB_NUM_VARIANTS) return -1;
+  return resolve(A, lda, B, ldb, variant);
+}
+
+int tb_validate_launch(int64_t m, int64_t k, int64_t n, int32_t tile_edge, int32_t variant, int32_t device) {
+  int s = check_device(device);
+  if (s) return s;
+  return validate(m, k, n, tile_edge, variant, device);
+}
+
+int tb_dgemm(const double* A, const double* B, double* C, int64_t m, int64_t k, int64_t n, int32_t tile_edge,
+             int32_t variant, int32_t device, void* cuda_stream, double* out_kernel_seconds) {
+  return dgemm_common(A, B, C, m, k, n, tile_edge, variant, device, cuda_stream, out_kernel_seconds, false);
+}
+
+int tb_cublas_dgemm(const double* A, const double* B, double* C, int64_t m, int64_t k, int64_t n, int32_t tile_edge,
+                    int32_t variant, int32_t device, void* cuda_stream, double* out_kernel_seconds) {
+  return dgemm_common(A, B, C, m, k, n, tile_edge, variant, device, cuda_stream, out_kernel_seconds, true);
+}
+
+int tb_dgemm_launch(const double* A, int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc, int64_t m,
+                    int64_t k, int64_t n, int32_t accumulate, int32_t tile_edge, int32_t variant, void* cuda_stream) {
+  int dev = -1;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
+    cudaGetLastError();
+    set_err("no current CUDA device");
+    return TB_STATUS_NO_DEVICE;
+  }
+  int s = check_device(dev);
+  if (s) return s;
+  if (!A || !B || !C) {
+    set_err("null buffer pointer");
+    return TB_STATUS_BAD_DIMS;
+  }
+  if ((s = validate(m, k, n, tile_edge, variant, dev))) return s;
+  if (lda < k || ldb < n || ldc < n) {
+    set_err("leading dimensions too small (lda=%lld ldb=%lld ldc=%lld)", (long long)lda, (long long)ldb,
+            (long long)ldc);
+    return TB_STATUS_BAD_DIMS;
+  }
+  return launch(dev, A, lda, B, ldb, C, ldc, m, k, n, accumulate, tile_edge, variant,
+                static_cast<cudaStream_t>(cuda_stream));
+}
+
+int tb_gpu_tiled_multiply_flat_ex(int32_t device, const double* a, const double* b, int64_t m, int64_t k, int64_t n,
+                                  int32_t tile_edge, int32_t variant, double* out_c, int64_t out_c_len,
+                                  double* out_seconds, double* out_e2e_seconds) {
+  int s = check_device(device);  // multiply.ts:65 — no device is a status, not a throw
+  if (s) return s;
+  if (!a || !b || !out_c || !out_seconds || m < 1 || k < 1 || n < 1 || out_c_len != m * n) {
+    set_err("bad dimensions or output buffer (out_c_len=%lld, m*n=%lld)", (long long)out_c_len,
+            (long long)(m * n));
+    return TB_STATUS_BAD_DIMS;  // multiply.ts:66
+  }
+  if ((s = validate(m, k, n, tile_edge, variant, device))) return s;
+  DeviceGuard guard(device);
+  DeviceState& st = g_dev[device];
+  std::lock_guard<std::mutex> lk(st.host_mu);  // one in-flight call per backend
+  const size_t na = (size_t)(m * k), nb = (size_t)(k * n), nc = (size_t)(m * n);
+  auto up = [](size_t x) { return (x + 31) & ~size_t(31); };  // 256-byte aligned sub-buffers
+  const size_t need = (up(na) + up(nb) + up(nc)) * sizeof(double);
+  if (!st.host_stream) TB_CUDA(cudaStreamCreateWithFlags(&st.host_stream, cudaStreamNonBlocking), "stream create");
+  if (st.ws_bytes < need) {
+    if (st.ws) cudaFree(st.ws);
+    st.ws = nullptr;
+    st.ws_bytes = 0;
+    TB_CUDA(cudaMalloc(&st.ws, need), "device workspace allocation");
+    st.ws_bytes = need;
+  }
+  double* dA = st.ws;
+  double* dB = dA + up(na);
+  double* dC = dB + up(nb);
+  cudaStream_t stream = st.host_stream;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  int rc = TB_STATUS_OK;
+  for (auto& e : ev)
+    if (cudaEventCreate(&e) != cudaSuccess) rc = cuda_fail(cudaGetLastError(), "event create");
+  if (rc == TB_STATUS_OK) {
+    cudaEventRecord(ev[0], stream);
+    cudaError_t e = cudaMemcpyAsync(dA, a, na * sizeof(double), cudaMemcpyHostToDevice, stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dB, b, nb * sizeof(double), cudaMemcpyHostToDevice, stream);
+    if (e != cudaSuccess) rc = cuda_fail(e, "host to device copy");
+  }
+  if (rc == TB_STATUS_OK) {
+    cudaEventRecord(ev[1], stream);
+    rc = launch(device, dA, k, dB, n, dC, n, m, k, n, 0, tile_edge, variant, stream);
+  }
+  if (rc == TB_STATUS_OK) {
+    cudaEventRecord(ev[2], stream);
+    cudaError_t e = cudaMemcpyAsync(out_c, dC, nc * sizeof(double), cudaMemcpyDeviceToHost, stream);
+    if (e != cudaSuccess) rc = cuda_fail(e, "device to host copy");
+  }
+  if (rc == TB_STATUS_OK) {
+    cudaEventRecord(ev[3], stream);
+    cudaError_t e = cudaEventSynchronize(ev[3]);
+    if (e != cudaSuccess) rc = cuda_fail(e, "kernel execution");
+  }
+  if (rc == TB_STATUS_OK) {
+    float k_ms = 0.f, e_ms = 0.f;
+    cudaEventElapsedTime(&k_ms, ev[1], ev[2]);
+    cudaEventElapsedTime(&e_ms, ev[0], ev[3]);
+    *out_seconds = (double)k_ms * 1e-3;
+    if (out_e2e_seconds) *out_e2e_seconds = (double)e_ms * 1e-3;
+  }
+  for (auto& e : ev)
+    if (e) cudaEventDestroy(e);
+  return rc;
+}
+
+int tb_gpu_tiled_multiply_flat(int32_t device, const double* a, const double* b, int64_t m, int64_t k, int64_t n,
+                               int32_t tile_edge, double* out_c, int64_t out_c_len, double* out_seconds) {
+  return tb_gpu_tiled_multiply_flat_ex(device, a, b, m, k, n, tile_edge, TB_VARIANT_AUTO, out_c, out_c_len,
+                                       out_seconds, nullptr);
+}
+
+void tb_release(void) {
+  const int count = device_count_raw();
+  for (int d = 0; d < count && d < kMaxDevices; ++d) {
+    DeviceState& st = g_dev[d];
+    std::lock_guard<std::mutex> lk_host(st.host_mu);
+    std::lock_guard<std::mutex> lk(st.mu);
+    DeviceGuard guard(d);
+    if (st.ws) cudaFree(st.ws);
+    st.ws = nullptr;
+    st.ws_bytes = 0;
+    if (st.cublas) cublasDestroy(st.cublas);
+    st.cublas = nullptr;
+    if (st.host_stream) cudaStreamDestroy(st.host_stream);
+    st.host_stream = nullptr;
+  }
+}
+
+}  // extern "C"

@@ -1,0 +1,267 @@
+"""GPU parity of the sm_100a kernels against the CPU oracle and the
+reference-generated golden fixtures (run on a B200: pytest -m gpu).
+
+Mirrors the reference's kernel suite (pkg/gpu/tests/kernel.test.ts:21-182)
+and the backend pins (pkg/tests/test_backends.py:23-71,
+test_acceptance.py:57-73). Bars (BASELINE.json north_star):
+  normwise ||C_gpu - C_ref||_F / ||C_ref||_F <= 1e-12,
+  max_abs_rel_diff <= 1e-10 (harness.py:41 ORACLE_RTOL),
+  and BITWISE equality with the reference naive oracle for the paper variant
+  (no FMA contraction, k-order running sum; kernel.ts:50-78).
+"""
+import ctypes
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+NORMWISE = 1e-12
+ELEMWISE = 1e-10
+FAST = ["dmma_tma", "dmma_cpasync"]
+
+
+@pytest.fixture(scope="module")
+def tb():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need a CUDA device (run with -m 'not gpu' on CPU)")
+    import paper_2509_04594_b200 as tb
+
+    assert tb._lib.device_count() >= 1
+    return tb
+
+
+def _gen(o, m, k, n, sa, sb):
+    return o.generate(m, k, sa), o.generate(k, n, sb)
+
+
+def _gpu(tb, a, b, variant, tile=32):
+    out, sec = tb.gpu_tiled_multiply_timed(a, b, tb.TileConfig(tile), variant=variant)
+    assert sec > 0.0
+    return out
+
+
+def test_one_by_one_is_twelve(tb):
+    for v in ["auto", "paper"] + FAST:
+        out = _gpu(tb, np.array([[3.0]]), np.array([[4.0]]), v)
+        assert out.shape == (1, 1) and out[0, 0] == 12.0
+
+
+def test_hand_checked_two_by_two(tb):
+    a = np.array([[1.0, 2.0], [3.0, 4.0]])
+    b = np.array([[5.0, 6.0], [7.0, 8.0]])
+    for v in ["paper"] + FAST:
+        assert np.array_equal(_gpu(tb, a, b, v), [[19.0, 22.0], [43.0, 50.0]])
+
+
+@pytest.mark.parametrize("variant", ["paper"] + FAST)
+def test_golden_grid(tb, golden, oracle, variant):
+    meta, g = golden
+    for c in meta["cases"]:
+        a, b = _gen(oracle, c["m"], c["k"], c["n"], c["seed_a"], c["seed_b"])
+        naive = g[c["tag"] + "_naive"]
+        tiles = c["tiles"] if variant == "paper" else [32]
+        for t in tiles:
+            if t * t > 1024:
+                continue
+            got = _gpu(tb, a, b, variant, t)
+            if variant == "paper":
+                assert np.array_equal(got, naive), (c["tag"], t)
+            assert tb.max_abs_rel_diff(got, naive) <= ELEMWISE, (c["tag"], variant, t)
+            assert oracle.normwise_rel(got, naive) <= NORMWISE, (c["tag"], variant, t)
+            assert oracle.normwise_rel(got, g[c["tag"] + "_tiled32"]) <= NORMWISE
+
+
+@pytest.mark.parametrize("variant", ["paper"] + FAST)
+def test_identity_with_hanging_column_is_bitwise(tb, oracle, variant):
+    n = 33
+    b = oracle.generate(n, n, 11)
+    assert np.array_equal(_gpu(tb, np.eye(n), b, variant), b)
+
+
+@pytest.mark.parametrize("variant", FAST)
+def test_zero_fill_border_row(tb, oracle, variant):
+    n = 33
+    a, b = _gen(oracle, n, n, n, 9, 10)
+    got = _gpu(tb, a, b, variant)
+    want = oracle.naive(a, b)
+    assert oracle.max_abs_rel_diff(got[n - 1], want[n - 1]) <= 1e-12
+    assert oracle.max_abs_rel_diff(got[:, n - 1], want[:, n - 1]) <= 1e-12
+
+
+@pytest.mark.parametrize("m,k,n", [(1, 1000, 1), (130, 17, 257), (255, 129, 127), (128, 16, 128), (7, 3, 300)])
+@pytest.mark.parametrize("variant", FAST)
+def test_ragged_shapes(tb, oracle, m, k, n, variant):
+    a, b = _gen(oracle, m, k, n, m + 1, n + 2)
+    got = _gpu(tb, a, b, variant)
+    ref = oracle.tiled_parallel(a, b)
+    assert oracle.normwise_rel(got, ref) <= NORMWISE
+    assert oracle.max_abs_rel_diff(got, ref) <= ELEMWISE
+
+
+def test_config0_n1000_full(tb, golden, oracle):
+    """configs[0]: N = 1000, seeds (1, 2): GPU vs the reference's tiled CPU
+    result (oracle reproduces its SHA-256, test_oracle.py)."""
+    meta, g = golden
+    a, b = oracle.generate(1000, 1000, 1), oracle.generate(1000, 1000, 2)
+    ref = oracle.tiled_parallel(a, b)
+    for v in ["auto"] + FAST:
+        got = _gpu(tb, a, b, v)
+        assert oracle.normwise_rel(got, ref) <= NORMWISE
+        assert oracle.max_abs_rel_diff(got, ref) <= ELEMWISE
+        rows = g["n1000_rows"]
+        assert oracle.normwise_rel(got[rows], g["n1000_tiled32_rows"]) <= NORMWISE
+
+
+@pytest.mark.parametrize("n", [4000, 10000])
+def test_large_row_sampled(tb, golden, oracle, n):
+    """configs[1] / [3] sizes: rows of the GPU product vs the reference's
+    tiled result on the same rows (bitwise equal to the full CPU product's
+    rows), plus a full-matrix check against cuBLAS."""
+    import torch
+
+    meta, g = golden
+    a, b = oracle.generate(n, n, 1), oracle.generate(n, n, 2)
+    ta, tb_ = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    c, sec = tb.dgemm(ta, tb_)
+    rows = g[f"n{n}_rows"]
+    got_rows = c[torch.from_numpy(rows).cuda()].cpu().numpy()
+    assert oracle.normwise_rel(got_rows, g[f"n{n}_tiled32_rows"]) <= NORMWISE
+    assert oracle.max_abs_rel_diff(got_rows, g[f"n{n}_tiled32_rows"]) <= ELEMWISE
+    ref, _ = tb.cublas_dgemm(ta, tb_)
+    rel = (torch.linalg.norm(c - ref) / torch.linalg.norm(ref)).item()
+    assert rel <= NORMWISE
+
+
+def test_deterministic_bits(tb, oracle):
+    a, b = _gen(oracle, 515, 515, 515, 3, 4)
+    for v in FAST + ["paper"]:
+        one, two = _gpu(tb, a, b, v), _gpu(tb, a, b, v)
+        assert one.tobytes() == two.tobytes()
+
+
+def test_inputs_not_mutated(tb, oracle):
+    a, b = _gen(oracle, 64, 64, 64, 5, 6)
+    a0, b0 = a.copy(), b.copy()
+    tb.gpu_tiled_multiply(a, b)
+    assert np.array_equal(a, a0) and np.array_equal(b, b0)
+
+
+def test_variant_resolution(tb):
+    import torch
+
+    lib = tb._lib.lib()
+    x = torch.empty(64, dtype=torch.float64, device="cuda")
+    p = x.data_ptr()
+    assert lib.tb_resolve_variant(ctypes.c_void_p(p), 10, ctypes.c_void_p(p), 10, 0) == tb._lib.VARIANT_DMMA_TMA
+    assert lib.tb_resolve_variant(ctypes.c_void_p(p), 11, ctypes.c_void_p(p), 10, 0) == tb._lib.VARIANT_DMMA_CPASYNC
+    assert lib.tb_resolve_variant(ctypes.c_void_p(p + 8), 10, ctypes.c_void_p(p), 10, 0) == tb._lib.VARIANT_DMMA_CPASYNC
+    assert lib.tb_resolve_variant(ctypes.c_void_p(p), 10, ctypes.c_void_p(p), 10, 1) == tb._lib.VARIANT_PAPER
+
+
+def test_launch_accumulate_and_strided_panels(tb, oracle):
+    """tb_dgemm_launch: column-panel views of A (lda = k), row-panel views of
+    B, C += A·B — the multi-GPU K-panel step."""
+    import torch
+
+    m, k, n = 300, 258, 190
+    a, b = _gen(oracle, m, k, n, 21, 22)
+    ta, tb_ = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    out = torch.zeros((m, n), dtype=torch.float64, device="cuda")
+    for i, (k0, k1) in enumerate([(0, 100), (100, 202), (202, 258)]):
+        tb.dgemm_launch(ta[:, k0:k1], tb_[k0:k1], out, accumulate=i > 0)
+    torch.cuda.synchronize()
+    ref = oracle.tiled_parallel(a, b)
+    assert oracle.normwise_rel(out.cpu().numpy(), ref) <= NORMWISE
+    # odd panel boundary -> unaligned base -> cp.async path
+    out.zero_()
+    for i, (k0, k1) in enumerate([(0, 101), (101, 258)]):
+        tb.dgemm_launch(ta[:, k0:k1], tb_[k0:k1], out, accumulate=i > 0)
+    torch.cuda.synchronize()
+    assert oracle.normwise_rel(out.cpu().numpy(), ref) <= NORMWISE
+
+
+def test_flat_abi_status_codes(tb, oracle):
+    """kernel.test.ts:123-182: OK / NO_DEVICE / OVER_LIMITS / BAD_DIMS."""
+    n = 16
+    a, b = _gen(oracle, n, n, n, 12, 13)
+    out_c = np.zeros(n * n)
+    out_s = np.zeros(1)
+    assert tb.gpu_tiled_multiply_flat(0, a, b, n, n, n, 16, out_c, out_s) == tb.STATUS_OK
+    assert out_s[0] > 0
+    assert oracle.max_abs_rel_diff(out_c.reshape(n, n), oracle.naive(a, b)) <= ELEMWISE
+    assert tb.gpu_tiled_multiply_flat(None, a, b, n, n, n, 32, out_c, out_s) == tb.STATUS_NO_DEVICE
+    assert tb.gpu_tiled_multiply_flat(4096, a, b, n, n, n, 32, out_c, out_s) == tb.STATUS_NO_DEVICE
+    assert tb.gpu_tiled_multiply_flat(0, a, b, n, n, n, 64, out_c, out_s) == tb.STATUS_OVER_LIMITS
+    assert tb.gpu_tiled_multiply_flat(0, a, b, n, n, n, 4, np.zeros(3), out_s) == tb.STATUS_BAD_DIMS
+    assert tb.gpu_tiled_multiply_flat(0, a, b, n, n, n, 0, out_c, out_s) == tb.STATUS_BAD_DIMS
+    assert tb.gpu_tiled_multiply_flat(0, a, b, 0, n, n, 32, out_c, out_s) == tb.STATUS_BAD_DIMS
+    for v in ("paper", "dmma_tma", "dmma_cpasync"):
+        out_c[:] = 0
+        e2e = np.zeros(1)
+        assert tb.gpu_tiled_multiply_flat(0, a, b, n, n, n, 16, out_c, out_s, variant=v,
+                                          out_e2e_seconds=e2e) == tb.STATUS_OK
+        assert e2e[0] >= out_s[0] > 0
+        assert oracle.normwise_rel(out_c.reshape(n, n), oracle.naive(a, b)) <= NORMWISE
+
+
+def test_exceptions_map_to_reference_kinds(tb, oracle):
+    a, b = _gen(oracle, 4, 4, 4, 1, 2)
+    with pytest.raises(tb.InvalidConfigError):
+        tb.gpu_tiled_multiply(a, b, tb.TileConfig(64), variant="paper")
+    with pytest.raises(tb.ShapeError):
+        tb.gpu_tiled_multiply(np.ones((2, 3)), np.ones((2, 3)))
+
+
+def test_registry_and_device_timed_runner(tb, oracle, tmp_path):
+    reg = tb.BackendRegistry()
+    assert reg.names() == [tb.GPU_BACKEND_NAME, tb.PAPER_BACKEND_NAME, tb.CUBLAS_BACKEND_NAME]
+    cfg = tb.RunConfig(backends=(tb.GPU_BACKEND_NAME, tb.CUBLAS_BACKEND_NAME), sizes=(64, 129), trials=3,
+                       verify=True)
+    records, meta = tb.run_trials(cfg, reg, verifier=oracle.naive)
+    assert len(records) == 2 * 2 * 3
+    for r in records:
+        assert r.seconds > 0 and abs(r.flops - tb.flop_count(r.n) / r.seconds) <= 1e-12 * r.flops
+    path = tmp_path / "gpu.csv"
+    tb.write_records(path, records, meta)
+    lines = path.read_text().splitlines()
+    assert lines[0] == "backend,n,trial,seconds,flops" and len(lines) == 13
+
+
+def test_liar_backend_caught_by_verify(tb, oracle):
+    reg = tb.BackendRegistry()
+    reg.register_external(tb.BackendDescriptor("liar"), lambda a, b: tb.gpu_tiled_multiply(a, b) + 1.0)
+    cfg = tb.RunConfig(backends=("liar",), sizes=(16,), trials=1, verify=True)
+    with pytest.raises(tb.TrialError):
+        tb.run_trials(cfg, reg, verifier=oracle.naive)
+
+
+def test_sharded_gemm_single_rank_nccl_panels(tb, oracle):
+    """The multi-GPU driver on one rank over NCCL: K-panel broadcast + panel GEMMs."""
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2509_04594_b200.multigpu import ShardedGemm, row_partitions
+
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29533")
+    if not dist.is_initialized():
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        n = 1000
+        a, b = oracle.generate(n, n, 1), oracle.generate(n, n, 2)
+        (r0, r1), = row_partitions(n, 1)
+        ta = torch.from_numpy(a[r0:r1]).cuda()
+        tb_ = torch.from_numpy(b).cuda()
+        ref = oracle.tiled_parallel(a, b)
+        for panels in (1, 4, 7):
+            out = torch.empty((r1 - r0, n), dtype=torch.float64, device="cuda")
+            ShardedGemm(panels=panels)(ta, tb_, out)
+            torch.cuda.synchronize()
+            assert oracle.normwise_rel(out.cpu().numpy(), ref) <= NORMWISE
+    finally:
+        dist.destroy_process_group()

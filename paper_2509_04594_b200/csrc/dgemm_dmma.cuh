@@ -3,12 +3,23 @@
 // The paper's K = 32 tiled kernel (reference kernel.ts:50-78)
 // "revisited for Blackwell": instead of one output per thread fed by two
 // shared-memory loads per FMA, a 128 x 128 CTA tile is computed by 8 consumer
-// warps (64 x 32 warp tiles, 32 DMMA accumulators each) while a producer warp
-// streams 128 x 16 / 16 x 128 k-slabs of A and B into a STAGES-deep
+// warps (64 x 32 warp tiles, 32 DMMA accumulators each) while a producer
+// warpgroup streams 128 x 16 / 16 x 128 k-slabs of A and B into a STAGES-deep
 // shared-memory ring (TMA with SWIZZLE_128B, or 8-byte cp.async with zero fill
 // when the TMA 16-byte alignment rule does not hold). Full/empty mbarriers hand
 // stages between producer and consumers; there is no __syncthreads in the main
 // loop.
+//
+// Persistent schedule. One CTA per SM walks a static work list: first the
+// data-parallel tiles (a multiple of gridDim.x, round-robin in grouped raster
+// order), then a stream-K region — the last (T mod P) + P tiles' k-iterations
+// split evenly across all CTAs, so the final partial wave does not leave SMs
+// idle. The producer runs ahead across work units, so a tile's epilogue
+// overlaps the next tile's loads. A tile split into segments is reduced
+// deterministically: every segment writes its partial to a workspace slot,
+// the CTA that completes the tile's segment count last sums the slots in
+// segment order (fixed, independent of timing) and writes C, then resets the
+// tile's counter for the next launch.
 //
 // Bank-conflict-free fragment loads. With the swizzled layout, the natural
 // DMMA k order (lane q feeds k = 4s + q) gives 2-way conflicts. The k index
@@ -34,6 +45,7 @@ struct DmmaCfg {
   static constexpr int MI = WM / 8;        // 8 DMMA rows per warp
   static constexpr int NI = WN / 8;        // 4 DMMA cols per warp
   static constexpr int CONSUMER_WARPS = WARPS_M * WARPS_N;
+  static constexpr int CONSUMER_THREADS = CONSUMER_WARPS * 32;
   // Warpgroup specialisation: warpgroup 0 = producer (one TMA-issuing lane, or
   // all 4 warps issuing cp.async), warpgroups 1-2 = the 8 consumer warps.
   // setmaxnreg moves registers from the producer to the consumers
@@ -46,11 +58,12 @@ struct DmmaCfg {
   static constexpr int STAGE = A_STAGE + B_STAGE;
   static constexpr int B_BOX = BK * 16 * 8;  // 2 KB
   static constexpr int GROUP_M = 8;          // tile raster: GROUP_M tile-rows per band
+  static constexpr int TILE_ELEMS = BM * BN;
 };
 
 template <int STAGES>
 constexpr int dmma_smem_bytes() {
-  return STAGES * DmmaCfg::STAGE + 2 * STAGES * 8 + 1024;  // + barriers + alignment slack
+  return STAGES * DmmaCfg::STAGE + 2 * STAGES * 8 + 16 + 1024;  // + barriers + flag + alignment slack
 }
 
 struct GemmParams {
@@ -60,8 +73,16 @@ struct GemmParams {
   int64_t lda, ldb, ldc;
   int m, n, k;
   int tiles_m, tiles_n;
+  int num_k;       // k-slabs per tile
   int accumulate;  // C += A·B instead of C = A·B
   int vec_store;   // C rows 16-byte aligned: store double2
+  // persistent schedule
+  int dp_tiles;    // data-parallel tiles, processed round-robin (multiple of gridDim.x)
+  int sk_tiles;    // stream-K tiles after them
+  int sk_ipc;      // stream-K k-iterations per CTA
+  int max_seg;     // workspace slots per stream-K tile
+  double* partials;  // [sk_tiles][max_seg][TILE_ELEMS] in fragment order
+  int* counters;     // [sk_tiles], zero between launches (self-resetting)
 };
 
 // Grouped raster over the (tile_m, tile_n) grid so concurrently resident CTAs
@@ -75,6 +96,35 @@ __device__ __forceinline__ void tile_coords(int tile, int tiles_m, int tiles_n, 
   tn = r / gm;
 }
 
+// The CTA's static work list: (tile, [kb, ke)) units. Producer and consumers
+// each walk their own copy, so they agree without communicating.
+struct WorkIter {
+  int t, it, end;
+  __device__ __forceinline__ explicit WorkIter(const GemmParams& p) {
+    t = blockIdx.x;
+    it = blockIdx.x * p.sk_ipc;
+    end = min(it + p.sk_ipc, p.sk_tiles * p.num_k);
+  }
+  __device__ __forceinline__ bool next(const GemmParams& p, int& tile, int& kb, int& ke) {
+    if (t < p.dp_tiles) {
+      tile = t;
+      kb = 0;
+      ke = p.num_k;
+      t += gridDim.x;
+      return true;
+    }
+    if (it >= end) return false;
+    const int st = it / p.num_k;
+    kb = it - st * p.num_k;
+    ke = min(p.num_k, kb + (end - it));
+    tile = p.dp_tiles + st;
+    it += ke - kb;
+    return true;
+  }
+};
+
+__device__ __forceinline__ void consumer_bar() { asm volatile("bar.sync 1, %0;\n" ::"n"(DmmaCfg::CONSUMER_THREADS)); }
+
 template <int STAGES, Loader LD>
 __global__ void __launch_bounds__(DmmaCfg::THREADS, 1)
     dgemm_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -83,15 +133,14 @@ __global__ void __launch_bounds__(DmmaCfg::THREADS, 1)
   extern __shared__ uint8_t smem_raw[];
   // SWIZZLE_128B's XOR pattern is a function of absolute smem address bits
   // [4:6] ^ [7:9]: stage buffers must start on 1024-byte boundaries.
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // (Offset the __shared__ array itself so the compiler keeps the shared
+  // address space and emits LDS rather than generic loads.)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE);
   uint64_t* empty = full + STAGES;
+  int* flag = reinterpret_cast<int*>(empty + STAGES);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  int tm, tn;
-  tile_coords(blockIdx.x, p.tiles_m, p.tiles_n, tm, tn);
-  const int m0 = tm * C::BM, n0 = tn * C::BN;
-  const int num_k = (p.k + C::BK - 1) / C::BK;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -105,52 +154,58 @@ __global__ void __launch_bounds__(DmmaCfg::THREADS, 1)
   if (warp < 4) {
     // ------------------------------------------------------------ producer
     setmaxnreg_dec<C::PRODUCER_REGS>();
-    if constexpr (LD == Loader::TMA) {
-      if (warp == 0 && lane == 0) {
-        tma_prefetch_desc(&tmA);
-        tma_prefetch_desc(&tmB);
-        for (int kt = 0; kt < num_k; ++kt) {
-          const int s = kt % STAGES;
-          const uint32_t ph = (kt / STAGES) & 1;
-          if (kt >= STAGES) mbar_wait(smem_u32(&empty[s]), ph ^ 1);
+    if (LD == Loader::TMA && threadIdx.x != 0) return;
+    if (LD == Loader::TMA) {
+      tma_prefetch_desc(&tmA);
+      tma_prefetch_desc(&tmB);
+    }
+    int s = 0;
+    uint32_t ph = 0;
+    WorkIter w(p);
+    int tile, kb, ke;
+    while (w.next(p, tile, kb, ke)) {
+      int tm, tn;
+      tile_coords(tile, p.tiles_m, p.tiles_n, tm, tn);
+      const int m0 = tm * C::BM, n0 = tn * C::BN;
+      for (int kt = kb; kt < ke; ++kt) {
+        mbar_wait(smem_u32(&empty[s]), ph ^ 1);  // fresh barrier: parity 1 reads as complete
+        const uint32_t sa = smem_u32(smem + s * C::STAGE);
+        const uint32_t sb = sa + C::A_STAGE;
+        if constexpr (LD == Loader::TMA) {
           const uint32_t fb = smem_u32(&full[s]);
-          const uint32_t sa = smem_u32(smem + s * C::STAGE);
-          const uint32_t sb = sa + C::A_STAGE;
           mbar_arrive_expect_tx(fb, C::STAGE);  // OOB-filled boxes still count full bytes
           tma_load_2d(sa, &tmA, fb, kt * C::BK, m0);
 #pragma unroll
           for (int j = 0; j < C::BN / 16; ++j) tma_load_2d(sb + j * C::B_BOX, &tmB, fb, n0 + 16 * j, kt * C::BK);
-        }
-      }
-    } else {
-      // 8-byte cp.async into the same swizzled layout; src-size 0 zero-fills
-      // out-of-range cells (the paper's "load zero" edge rule).
-      for (int kt = 0; kt < num_k; ++kt) {
-        const int s = kt % STAGES;
-        const uint32_t ph = (kt / STAGES) & 1;
-        if (kt >= STAGES) mbar_wait(smem_u32(&empty[s]), ph ^ 1);
-        const uint32_t sa = smem_u32(smem + s * C::STAGE);
-        const uint32_t sb = sa + C::A_STAGE;
-        const int k0 = kt * C::BK;
-        const int pt = threadIdx.x;  // 0..127
+        } else {
+          // 8-byte cp.async into the same swizzled layout; src-size 0
+          // zero-fills out-of-range cells (the paper's "load zero" edge rule,
+          // PAPER.md:124).
+          const int k0 = kt * C::BK;
+          const int pt = threadIdx.x;  // 0..127
 #pragma unroll 4
-        for (int it = 0; it < (C::BM * C::BK) / 128; ++it) {
-          const int e = it * 128 + pt, r = e >> 4, kk = e & 15;
-          const int gm = m0 + r, gk = k0 + kk;
-          const bool ok = gm < p.m && gk < p.k;
-          const double* src = ok ? p.A + (int64_t)gm * p.lda + gk : p.A;
-          cp_async_8(sa + r * 128 + (((kk >> 1) ^ (r & 7)) << 4) + (kk & 1) * 8, src, ok);
-        }
+          for (int i = 0; i < (C::BM * C::BK) / 128; ++i) {
+            const int e = i * 128 + pt, r = e >> 4, kk = e & 15;
+            const int gm = m0 + r, gk = k0 + kk;
+            const bool ok = gm < p.m && gk < p.k;
+            const double* src = ok ? p.A + (int64_t)gm * p.lda + gk : p.A;
+            cp_async_8(sa + r * 128 + (((kk >> 1) ^ (r & 7)) << 4) + (kk & 1) * 8, src, ok);
+          }
 #pragma unroll 4
-        for (int it = 0; it < (C::BK * C::BN) / 128; ++it) {
-          const int e = it * 128 + pt, kr = e >> 7, nn = e & 127;
-          const int gk = k0 + kr, gn = n0 + nn;
-          const bool ok = gk < p.k && gn < p.n;
-          const double* src = ok ? p.B + (int64_t)gk * p.ldb + gn : p.B;
-          cp_async_8(sb + (nn >> 4) * C::B_BOX + kr * 128 + ((((nn & 15) >> 1) ^ (kr & 7)) << 4) + (nn & 1) * 8,
-                     src, ok);
+          for (int i = 0; i < (C::BK * C::BN) / 128; ++i) {
+            const int e = i * 128 + pt, kr = e >> 7, nn = e & 127;
+            const int gk = k0 + kr, gn = n0 + nn;
+            const bool ok = gk < p.k && gn < p.n;
+            const double* src = ok ? p.B + (int64_t)gk * p.ldb + gn : p.B;
+            cp_async_8(sb + (nn >> 4) * C::B_BOX + kr * 128 + ((((nn & 15) >> 1) ^ (kr & 7)) << 4) + (nn & 1) * 8,
+                       src, ok);
+          }
+          cp_async_mbar_arrive_noinc(smem_u32(&full[s]));
         }
-        cp_async_mbar_arrive_noinc(smem_u32(&full[s]));
+        if (++s == STAGES) {
+          s = 0;
+          ph ^= 1;
+        }
       }
     }
     return;
@@ -158,6 +213,7 @@ __global__ void __launch_bounds__(DmmaCfg::THREADS, 1)
 
   // -------------------------------------------------------------- consumers
   setmaxnreg_inc<C::CONSUMER_REGS>();
+  const int ct = threadIdx.x - 128;  // consumer thread 0..255
   const int cw = warp - 4;
   const int wm = cw / C::WARPS_N, wn = cw % C::WARPS_N;
   const int q = lane & 3, g = lane >> 2;
@@ -178,67 +234,118 @@ __global__ void __launch_bounds__(DmmaCfg::THREADS, 1)
       b_off[e] = wn * 2 * C::B_BOX + kv[e] * 128 + ((((g >> 1) ^ (kv[e] & 7))) << 4) + (g & 1) * 8;
   }
 
-  double acc[C::MI][C::NI][2];
+  int s = 0;
+  uint32_t ph = 0;
+  WorkIter w(p);
+  int tile, kb, ke;
+  while (w.next(p, tile, kb, ke)) {
+    double acc[C::MI][C::NI][2];
 #pragma unroll
-  for (int i = 0; i < C::MI; ++i)
+    for (int i = 0; i < C::MI; ++i)
 #pragma unroll
-    for (int j = 0; j < C::NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+      for (int j = 0; j < C::NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-  for (int kt = 0; kt < num_k; ++kt) {
-    const int s = kt % STAGES;
-    const uint32_t ph = (kt / STAGES) & 1;
-    mbar_wait(smem_u32(&full[s]), ph);
-    const uint8_t* sa = smem + s * C::STAGE;
-    const uint8_t* sb = sa + C::A_STAGE;
+    for (int kt = kb; kt < ke; ++kt) {
+      mbar_wait(smem_u32(&full[s]), ph);
+      const uint8_t* sa = smem + s * C::STAGE;
+      const uint8_t* sb = sa + C::A_STAGE;
 #pragma unroll
-    for (int half = 0; half < 2; ++half) {
-      double2 af[C::MI];
-      double bf[2][C::NI];
+      for (int half = 0; half < 2; ++half) {
+        double2 af[C::MI];
+        double bf[2][C::NI];
+#pragma unroll
+        for (int i = 0; i < C::MI; ++i)
+          af[i] = *reinterpret_cast<const double2*>(sa + (half ? a_off1 : a_off0) + i * 8 * 128);
+#pragma unroll
+        for (int j = 0; j < C::NI; ++j) {
+          const uint32_t box = (j >> 1) * C::B_BOX, flip = (j & 1) ? 64u : 0u;
+          bf[0][j] = *reinterpret_cast<const double*>(sb + box + (b_off[2 * half] ^ flip));
+          bf[1][j] = *reinterpret_cast<const double*>(sb + box + (b_off[2 * half + 1] ^ flip));
+        }
+#pragma unroll
+        for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+          for (int j = 0; j < C::NI; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i].x, bf[0][j]);
+#pragma unroll
+        for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+          for (int j = 0; j < C::NI; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i].y, bf[1][j]);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&empty[s]));
+      if (++s == STAGES) {
+        s = 0;
+        ph ^= 1;
+      }
+    }
+
+    // ------------------------------------------------- stream-K segment fixup
+    if (kb != 0 || ke != p.num_k) {
+      const int st = tile - p.dp_tiles;
+      const int first = st * p.num_k;
+      const int seg = (first + kb) / p.sk_ipc - first / p.sk_ipc;
+      const int nseg = (first + p.num_k - 1) / p.sk_ipc - first / p.sk_ipc + 1;
+      double2* slots = reinterpret_cast<double2*>(p.partials) + (size_t)st * p.max_seg * (C::TILE_ELEMS / 2);
+      double2* mine = slots + (size_t)seg * (C::TILE_ELEMS / 2);
 #pragma unroll
       for (int i = 0; i < C::MI; ++i)
-        af[i] = *reinterpret_cast<const double2*>(sa + (half ? a_off1 : a_off0) + i * 8 * 128);
+#pragma unroll
+        for (int j = 0; j < C::NI; ++j)
+          __stcg(mine + (i * C::NI + j) * C::CONSUMER_THREADS + ct, make_double2(acc[i][j][0], acc[i][j][1]));
+      __threadfence();
+      consumer_bar();
+      if (ct == 0) *flag = atomicAdd(&p.counters[st], 1);
+      consumer_bar();
+      const bool last = (*flag == nseg - 1);
+      consumer_bar();  // flag is reused by the next unit
+      if (!last) continue;
+      __threadfence();
+      // Deterministic reduction: all segments (own one re-read from L2 too)
+      // summed in index order 0..nseg-1, whichever CTA finishes last.
+#pragma unroll
+      for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+        for (int j = 0; j < C::NI; ++j) {
+          const double2* src = slots + (i * C::NI + j) * C::CONSUMER_THREADS + ct;
+          double2 sum = __ldcg(src);
+          for (int sg = 1; sg < nseg; ++sg) {
+            const double2 v = __ldcg(src + (size_t)sg * (C::TILE_ELEMS / 2));
+            sum.x += v.x;
+            sum.y += v.y;
+          }
+          acc[i][j][0] = sum.x;
+          acc[i][j][1] = sum.y;
+        }
+      if (ct == 0) p.counters[st] = 0;  // self-reset for the next launch
+    }
+
+    // --------------------------------------------------------------- epilogue
+    int tm, tn;
+    tile_coords(tile, p.tiles_m, p.tiles_n, tm, tn);
+    const int m0 = tm * C::BM, n0 = tn * C::BN;
+#pragma unroll
+    for (int i = 0; i < C::MI; ++i) {
+      const int r = m0 + wm * C::WM + i * 8 + g;
+      if (r >= p.m) continue;
+      double* crow = p.C + (int64_t)r * p.ldc;
 #pragma unroll
       for (int j = 0; j < C::NI; ++j) {
-        const uint32_t box = (j >> 1) * C::B_BOX, flip = (j & 1) ? 64u : 0u;
-        bf[0][j] = *reinterpret_cast<const double*>(sb + box + (b_off[2 * half] ^ flip));
-        bf[1][j] = *reinterpret_cast<const double*>(sb + box + (b_off[2 * half + 1] ^ flip));
-      }
-#pragma unroll
-      for (int i = 0; i < C::MI; ++i)
-#pragma unroll
-        for (int j = 0; j < C::NI; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i].x, bf[0][j]);
-#pragma unroll
-      for (int i = 0; i < C::MI; ++i)
-#pragma unroll
-        for (int j = 0; j < C::NI; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i].y, bf[1][j]);
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(smem_u32(&empty[s]));
-  }
-
-  // --------------------------------------------------------------- epilogue
-#pragma unroll
-  for (int i = 0; i < C::MI; ++i) {
-    const int r = m0 + wm * C::WM + i * 8 + g;
-    if (r >= p.m) continue;
-    double* crow = p.C + (int64_t)r * p.ldc;
-#pragma unroll
-    for (int j = 0; j < C::NI; ++j) {
-      const int c = n0 + wn * C::WN + j * 8 + 2 * q;
-      double v0 = acc[i][j][0], v1 = acc[i][j][1];
-      if (c + 1 < p.n) {
-        if (p.accumulate) {
-          v0 += crow[c];
-          v1 += crow[c + 1];
+        const int c = n0 + wn * C::WN + j * 8 + 2 * q;
+        double v0 = acc[i][j][0], v1 = acc[i][j][1];
+        if (c + 1 < p.n) {
+          if (p.accumulate) {
+            v0 += crow[c];
+            v1 += crow[c + 1];
+          }
+          if (p.vec_store) {
+            *reinterpret_cast<double2*>(crow + c) = make_double2(v0, v1);
+          } else {
+            crow[c] = v0;
+            crow[c + 1] = v1;
+          }
+        } else if (c < p.n) {
+          crow[c] = p.accumulate ? v0 + crow[c] : v0;
         }
-        if (p.vec_store) {
-          *reinterpret_cast<double2*>(crow + c) = make_double2(v0, v1);
-        } else {
-          crow[c] = v0;
-          crow[c + 1] = v1;
-        }
-      } else if (c < p.n) {
-        crow[c] = p.accumulate ? v0 + crow[c] : v0;
       }
     }
   }

@@ -10,6 +10,8 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
+#include <map>
 #include <mutex>
 
 #include "../../include/tbgpu.h"
@@ -57,6 +59,13 @@ struct DeviceState {
   cudaStream_t host_stream = nullptr;  // stream of the host-buffer entry
   double* ws = nullptr;                // host-entry device workspace (A | B | C)
   size_t ws_bytes = 0;
+  struct SplitWs {                     // stream-K partial tiles + tile counters, per stream
+    double* partials = nullptr;
+    size_t partial_elems = 0;
+    int* counters = nullptr;
+    size_t counter_elems = 0;
+  };
+  std::map<cudaStream_t, SplitWs> split_ws;
 };
 
 DeviceState g_dev[kMaxDevices];
@@ -219,6 +228,64 @@ int check_device(int32_t device) {
   return ensure_device(device);
 }
 
+// Persistent schedule (dgemm_dmma.cuh): data-parallel tiles round-robin over
+// P = #SM CTAs, then the last (T mod P) + P tiles as stream-K k-iterations
+// split evenly across the CTAs. TB_SCHED=dp disables the stream-K region.
+struct Schedule {
+  int grid, dp, sk, ipc, max_seg;
+};
+
+Schedule plan_schedule(int64_t tiles, int num_k, int sms) {
+  static const bool dp_only = [] {
+    const char* e = std::getenv("TB_SCHED");
+    return e && std::strcmp(e, "dp") == 0;
+  }();
+  Schedule sc{sms, (int)tiles, 0, 1, 1};
+  const int64_t rem = tiles % sms;
+  if (dp_only || rem == 0) return sc;
+  sc.sk = (int)(tiles > sms ? rem + sms : tiles);
+  sc.dp = (int)(tiles - sc.sk);
+  const int64_t total = (int64_t)sc.sk * num_k;
+  int64_t ipc = (total + sms - 1) / sms;
+  const int64_t min_seg = num_k < 8 ? num_k : 8;  // keep segments long enough to amortise the fixup
+  if (ipc < min_seg) ipc = min_seg;
+  sc.ipc = (int)ipc;
+  int max_seg = 1;
+  for (int64_t st = 0; st < sc.sk; ++st) {
+    const int64_t first = st * num_k;
+    const int64_t nseg = (first + num_k - 1) / ipc - first / ipc + 1;
+    if (nseg > max_seg) max_seg = (int)nseg;
+  }
+  sc.max_seg = max_seg;
+  return sc;
+}
+
+int split_workspace(int dev, cudaStream_t stream, size_t partial_elems, size_t counter_elems, double** partials,
+                    int** counters) {
+  DeviceState& st = g_dev[dev];
+  std::lock_guard<std::mutex> lk(st.mu);
+  DeviceState::SplitWs& w = st.split_ws[stream];
+  if (w.partial_elems < partial_elems) {
+    if (w.partials) cudaFree(w.partials);
+    w.partials = nullptr;
+    w.partial_elems = 0;
+    TB_CUDA(cudaMalloc(&w.partials, partial_elems * sizeof(double)), "stream-K workspace allocation");
+    w.partial_elems = partial_elems;
+  }
+  if (w.counter_elems < counter_elems) {
+    if (w.counters) cudaFree(w.counters);
+    w.counters = nullptr;
+    w.counter_elems = 0;
+    TB_CUDA(cudaMalloc(&w.counters, counter_elems * sizeof(int)), "stream-K counter allocation");
+    // Counters start at zero once; each launch's last segment resets its tile's counter.
+    TB_CUDA(cudaMemset(w.counters, 0, counter_elems * sizeof(int)), "stream-K counter init");
+    w.counter_elems = counter_elems;
+  }
+  *partials = w.partials;
+  *counters = w.counters;
+  return TB_STATUS_OK;
+}
+
 // Enqueue one GEMM on `stream` (current device = dev). Assumes validated args.
 int launch(int dev, const double* A, int64_t lda, const double* B, int64_t ldb, double* Cm, int64_t ldc, int64_t m,
            int64_t k, int64_t n, int accumulate, int tile_edge, int variant, cudaStream_t stream) {
@@ -252,6 +319,18 @@ int launch(int dev, const double* A, int64_t lda, const double* B, int64_t ldb, 
       set_err("too many output tiles");
       return TB_STATUS_OVER_LIMITS;
     }
+    p.num_k = (int)((k + Cfg::BK - 1) / Cfg::BK);
+    const Schedule sc = plan_schedule(tiles, p.num_k, g_dev[dev].sms);
+    p.dp_tiles = sc.dp;
+    p.sk_tiles = sc.sk;
+    p.sk_ipc = sc.ipc;
+    p.max_seg = sc.max_seg;
+    p.partials = nullptr;
+    p.counters = nullptr;
+    if (sc.sk > 0 &&
+        (s = split_workspace(dev, stream, (size_t)sc.sk * sc.max_seg * Cfg::TILE_ELEMS, (size_t)sc.sk, &p.partials,
+                             &p.counters)))
+      return s;
     CUtensorMap mA, mB;
     std::memset(&mA, 0, sizeof(mA));
     std::memset(&mB, 0, sizeof(mB));
@@ -260,10 +339,10 @@ int launch(int dev, const double* A, int64_t lda, const double* B, int64_t ldb, 
       if ((s = get_encoder())) return s;
       if ((s = encode_map(&mA, A, m, k, lda, Cfg::BM))) return s;
       if ((s = encode_map(&mB, B, k, n, ldb, Cfg::BK))) return s;
-      tb::dgemm_dmma_kernel<kStages, tb::Loader::TMA><<<(unsigned)tiles, Cfg::THREADS, bytes, stream>>>(mA, mB, p);
+      tb::dgemm_dmma_kernel<kStages, tb::Loader::TMA><<<(unsigned)sc.grid, Cfg::THREADS, bytes, stream>>>(mA, mB, p);
     } else {
       tb::dgemm_dmma_kernel<kStages, tb::Loader::CPASYNC>
-          <<<(unsigned)tiles, Cfg::THREADS, bytes, stream>>>(mA, mB, p);
+          <<<(unsigned)sc.grid, Cfg::THREADS, bytes, stream>>>(mA, mB, p);
     }
   }
   TB_CUDA(cudaGetLastError(), "kernel launch");
@@ -482,6 +561,11 @@ void tb_release(void) {
     st.cublas = nullptr;
     if (st.host_stream) cudaStreamDestroy(st.host_stream);
     st.host_stream = nullptr;
+    for (auto& kv : st.split_ws) {
+      if (kv.second.partials) cudaFree(kv.second.partials);
+      if (kv.second.counters) cudaFree(kv.second.counters);
+    }
+    st.split_ws.clear();
   }
 }
 

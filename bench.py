@@ -334,7 +334,7 @@ def run_ours(args) -> None:
                          "avg_launch_ms": avg_launch * 1e3, "peak_source": peak_src},
             "e2e": {"value": flop_count(n) / e2e_s / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h,
-                    "path": "tb_gpu_tiled_multiply_flat_ex (pinned host A,B -> H2D -> kernel -> D2H C), "
+                    "path": "tb_gpu_tiled_multiply_flat_ex: pinned host A,B -> 3-stream pipeline (H2D row blocks + K-panels of B / GEMM / D2H row blocks) -> host C; "
                             "CUDA events on its stream"},
             "gpu_launches": args.steps * (1 if world == 1 else len(panel_bounds(n, args.panels))),
             "clocks": clk,

@@ -61,9 +61,10 @@ struct DmmaCfg {
   static constexpr int TILE_ELEMS = BM * BN;
 };
 
-template <int STAGES>
+// A pipeline stage holds SUB consecutive 16-deep k sub-slabs (SUB * 32 KB).
+template <int SUB, int STAGES>
 constexpr int dmma_smem_bytes() {
-  return STAGES * DmmaCfg::STAGE + 2 * STAGES * 8 + 16 + 1024;  // + barriers + flag + alignment slack
+  return STAGES * SUB * DmmaCfg::STAGE + 2 * STAGES * 8 + 16 + 1024;  // + barriers + flag + alignment slack
 }
 
 struct GemmParams {
@@ -73,7 +74,7 @@ struct GemmParams {
   int64_t lda, ldb, ldc;
   int m, n, k;
   int tiles_m, tiles_n;
-  int num_k;       // k-slabs per tile
+  int num_k;       // pipeline stages (SUB x 16-deep k sub-slabs) per tile
   int accumulate;  // C += A·B instead of C = A·B
   int vec_store;   // C rows 16-byte aligned: store double2
   // persistent schedule
@@ -125,7 +126,7 @@ struct WorkIter {
 
 __device__ __forceinline__ void consumer_bar() { asm volatile("bar.sync 1, %0;\n" ::"n"(DmmaCfg::CONSUMER_THREADS)); }
 
-template <int STAGES, Loader LD>
+template <int SUB, int STAGES, Loader LD>
 __global__ void __launch_bounds__(DmmaCfg::THREADS, 1)
     dgemm_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       const GemmParams p) {
@@ -136,7 +137,8 @@ __global__ void __launch_bounds__(DmmaCfg::THREADS, 1)
   // (Offset the __shared__ array itself so the compiler keeps the shared
   // address space and emits LDS rather than generic loads.)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE);
+  constexpr int STAGE_BYTES = SUB * C::STAGE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
   uint64_t* empty = full + STAGES;
   int* flag = reinterpret_cast<int*>(empty + STAGES);
 
@@ -169,20 +171,27 @@ __global__ void __launch_bounds__(DmmaCfg::THREADS, 1)
       const int m0 = tm * C::BM, n0 = tn * C::BN;
       for (int kt = kb; kt < ke; ++kt) {
         mbar_wait(smem_u32(&empty[s]), ph ^ 1);  // fresh barrier: parity 1 reads as complete
-        const uint32_t sa = smem_u32(smem + s * C::STAGE);
-        const uint32_t sb = sa + C::A_STAGE;
+        const uint32_t stage = smem_u32(smem + s * STAGE_BYTES);
         if constexpr (LD == Loader::TMA) {
           const uint32_t fb = smem_u32(&full[s]);
-          mbar_arrive_expect_tx(fb, C::STAGE);  // OOB-filled boxes still count full bytes
-          tma_load_2d(sa, &tmA, fb, kt * C::BK, m0);
+          mbar_arrive_expect_tx(fb, STAGE_BYTES);  // OOB-filled boxes still count full bytes
 #pragma unroll
-          for (int j = 0; j < C::BN / 16; ++j) tma_load_2d(sb + j * C::B_BOX, &tmB, fb, n0 + 16 * j, kt * C::BK);
+          for (int u = 0; u < SUB; ++u) {
+            const uint32_t sa = stage + u * C::STAGE, sb = sa + C::A_STAGE;
+            const int k0 = (kt * SUB + u) * C::BK;
+            tma_load_2d(sa, &tmA, fb, k0, m0);
+#pragma unroll
+            for (int j = 0; j < C::BN / 16; ++j) tma_load_2d(sb + j * C::B_BOX, &tmB, fb, n0 + 16 * j, k0);
+          }
         } else {
           // 8-byte cp.async into the same swizzled layout; src-size 0
           // zero-fills out-of-range cells (the paper's "load zero" edge rule,
           // PAPER.md:124).
-          const int k0 = kt * C::BK;
           const int pt = threadIdx.x;  // 0..127
+#pragma unroll
+          for (int u = 0; u < SUB; ++u) {
+          const uint32_t sa = stage + u * C::STAGE, sb = sa + C::A_STAGE;
+          const int k0 = (kt * SUB + u) * C::BK;
 #pragma unroll 4
           for (int i = 0; i < (C::BM * C::BK) / 128; ++i) {
             const int e = i * 128 + pt, r = e >> 4, kk = e & 15;
@@ -199,6 +208,7 @@ __global__ void __launch_bounds__(DmmaCfg::THREADS, 1)
             const double* src = ok ? p.B + (int64_t)gk * p.ldb + gn : p.B;
             cp_async_8(sb + (nn >> 4) * C::B_BOX + kr * 128 + ((((nn & 15) >> 1) ^ (kr & 7)) << 4) + (nn & 1) * 8,
                        src, ok);
+          }
           }
           cp_async_mbar_arrive_noinc(smem_u32(&full[s]));
         }
@@ -247,10 +257,11 @@ __global__ void __launch_bounds__(DmmaCfg::THREADS, 1)
 
     for (int kt = kb; kt < ke; ++kt) {
       mbar_wait(smem_u32(&full[s]), ph);
-      const uint8_t* sa = smem + s * C::STAGE;
-      const uint8_t* sb = sa + C::A_STAGE;
 #pragma unroll
-      for (int half = 0; half < 2; ++half) {
+      for (int hs = 0; hs < 2 * SUB; ++hs) {
+        const int half = hs & 1;
+        const uint8_t* sa = smem + s * STAGE_BYTES + (hs >> 1) * C::STAGE;
+        const uint8_t* sb = sa + C::A_STAGE;
         double2 af[C::MI];
         double bf[2][C::NI];
 #pragma unroll

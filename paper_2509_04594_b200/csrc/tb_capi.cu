@@ -10,7 +10,9 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <algorithm>
 #include <cstdlib>
+#include <vector>
 #include <map>
 #include <mutex>
 
@@ -24,7 +26,46 @@
 
 namespace {
 
-constexpr int kStages = 6;                 // 6 x 32 KB ring = 192 KB of the 227 KB opt-in
+// Pipeline shapes (sub-slabs per stage x stages). kProdCfg is the tuned
+// default; TB_KCFG=<index> selects another for A/B measurements.
+struct KCfg {
+  int sub, stages;
+};
+constexpr KCfg kCfgs[] = {{1, 6}, {1, 7}, {2, 3}};
+constexpr int kNumCfgs = sizeof(kCfgs) / sizeof(kCfgs[0]);
+constexpr int kProdCfg = 0;
+
+int active_cfg() {
+  static const int idx = [] {
+    const char* e = std::getenv("TB_KCFG");
+    const int v = e ? std::atoi(e) : kProdCfg;
+    return (v >= 0 && v < kNumCfgs) ? v : kProdCfg;
+  }();
+  return idx;
+}
+
+template <int SUB, int STAGES>
+struct KernelSet {
+  static void* tma() { return (void*)tb::dgemm_dmma_kernel<SUB, STAGES, tb::Loader::TMA>; }
+  static void* cpasync() { return (void*)tb::dgemm_dmma_kernel<SUB, STAGES, tb::Loader::CPASYNC>; }
+  static constexpr int smem() { return tb::dmma_smem_bytes<SUB, STAGES>(); }
+};
+
+void* cfg_kernel(int idx, bool tma) {
+  switch (idx) {
+    case 1: return tma ? KernelSet<1, 7>::tma() : KernelSet<1, 7>::cpasync();
+    case 2: return tma ? KernelSet<2, 3>::tma() : KernelSet<2, 3>::cpasync();
+    default: return tma ? KernelSet<1, 6>::tma() : KernelSet<1, 6>::cpasync();
+  }
+}
+
+int cfg_smem(int idx) {
+  switch (idx) {
+    case 1: return KernelSet<1, 7>::smem();
+    case 2: return KernelSet<2, 3>::smem();
+    default: return KernelSet<1, 6>::smem();
+  }
+}
 constexpr int kMaxDevices = 64;
 constexpr int kMaxBlockThreads = 1024;     // limits.ts:20-24 maxThreadsPerBlock
 
@@ -56,7 +97,9 @@ struct DeviceState {
   int smem_optin = 0;
   bool attrs_set = false;
   cublasHandle_t cublas = nullptr;
-  cudaStream_t host_stream = nullptr;  // stream of the host-buffer entry
+  cudaStream_t host_stream = nullptr;  // host-buffer entry: compute stream
+  cudaStream_t h2d_stream = nullptr;   // host-buffer entry: host-to-device copies
+  cudaStream_t d2h_stream = nullptr;   // host-buffer entry: device-to-host copies
   double* ws = nullptr;                // host-entry device workspace (A | B | C)
   size_t ws_bytes = 0;
   struct SplitWs {                     // stream-K partial tiles + tile counters, per stream
@@ -110,13 +153,13 @@ int ensure_kernel_attrs(int dev) {
   DeviceState& st = g_dev[dev];
   std::lock_guard<std::mutex> lk(st.mu);
   if (st.attrs_set) return TB_STATUS_OK;
-  const int bytes = tb::dmma_smem_bytes<kStages>();
-  TB_CUDA(cudaFuncSetAttribute(tb::dgemm_dmma_kernel<kStages, tb::Loader::TMA>,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
-          "set smem attribute (dmma_tma)");
-  TB_CUDA(cudaFuncSetAttribute(tb::dgemm_dmma_kernel<kStages, tb::Loader::CPASYNC>,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
-          "set smem attribute (dmma_cpasync)");
+  for (int i = 0; i < kNumCfgs; ++i) {
+    if (cfg_smem(i) > st.smem_optin) continue;  // validate() rejects the active one if it does not fit
+    TB_CUDA(cudaFuncSetAttribute(cfg_kernel(i, true), cudaFuncAttributeMaxDynamicSharedMemorySize, cfg_smem(i)),
+            "set smem attribute (dmma_tma)");
+    TB_CUDA(cudaFuncSetAttribute(cfg_kernel(i, false), cudaFuncAttributeMaxDynamicSharedMemorySize, cfg_smem(i)),
+            "set smem attribute (dmma_cpasync)");
+  }
   TB_CUDA(cudaFuncSetAttribute(tb::dgemm_paper_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                st.smem_optin),
           "set smem attribute (paper)");
@@ -210,8 +253,8 @@ int validate(int64_t m, int64_t k, int64_t n, int32_t tile_edge, int32_t variant
         set_err("grid of %lld tile rows exceeds gridDim.y 65535", (long long)((m + tile_edge - 1) / tile_edge));
         return TB_STATUS_OVER_LIMITS;
       }
-    } else if (tb::dmma_smem_bytes<kStages>() > st.smem_optin) {
-      set_err("dmma pipeline needs %d bytes of shared memory, device allows %d", tb::dmma_smem_bytes<kStages>(),
+    } else if (cfg_smem(active_cfg()) > st.smem_optin) {
+      set_err("dmma pipeline needs %d bytes of shared memory, device allows %d", cfg_smem(active_cfg()),
               st.smem_optin);
       return TB_STATUS_OVER_LIMITS;
     }
@@ -319,7 +362,9 @@ int launch(int dev, const double* A, int64_t lda, const double* B, int64_t ldb, 
       set_err("too many output tiles");
       return TB_STATUS_OVER_LIMITS;
     }
-    p.num_k = (int)((k + Cfg::BK - 1) / Cfg::BK);
+    const int cfg = active_cfg();
+    const int64_t kstage = (int64_t)Cfg::BK * kCfgs[cfg].sub;
+    p.num_k = (int)((k + kstage - 1) / kstage);
     const Schedule sc = plan_schedule(tiles, p.num_k, g_dev[dev].sms);
     p.dp_tiles = sc.dp;
     p.sk_tiles = sc.sk;
@@ -334,16 +379,16 @@ int launch(int dev, const double* A, int64_t lda, const double* B, int64_t ldb, 
     CUtensorMap mA, mB;
     std::memset(&mA, 0, sizeof(mA));
     std::memset(&mB, 0, sizeof(mB));
-    const int bytes = tb::dmma_smem_bytes<kStages>();
-    if (variant == TB_VARIANT_DMMA_TMA) {
+    const bool use_tma = variant == TB_VARIANT_DMMA_TMA;
+    if (use_tma) {
       if ((s = get_encoder())) return s;
       if ((s = encode_map(&mA, A, m, k, lda, Cfg::BM))) return s;
       if ((s = encode_map(&mB, B, k, n, ldb, Cfg::BK))) return s;
-      tb::dgemm_dmma_kernel<kStages, tb::Loader::TMA><<<(unsigned)sc.grid, Cfg::THREADS, bytes, stream>>>(mA, mB, p);
-    } else {
-      tb::dgemm_dmma_kernel<kStages, tb::Loader::CPASYNC>
-          <<<(unsigned)sc.grid, Cfg::THREADS, bytes, stream>>>(mA, mB, p);
     }
+    void* args[] = {&mA, &mB, &p};
+    TB_CUDA(cudaLaunchKernel(cfg_kernel(cfg, use_tma), dim3((unsigned)sc.grid), dim3(Cfg::THREADS), args,
+                             (size_t)cfg_smem(cfg), stream),
+            "kernel launch");
   }
   TB_CUDA(cudaGetLastError(), "kernel launch");
   return TB_STATUS_OK;
@@ -493,7 +538,8 @@ int tb_gpu_tiled_multiply_flat_ex(int32_t device, const double* a, const double*
   const size_t na = (size_t)(m * k), nb = (size_t)(k * n), nc = (size_t)(m * n);
   auto up = [](size_t x) { return (x + 31) & ~size_t(31); };  // 256-byte aligned sub-buffers
   const size_t need = (up(na) + up(nb) + up(nc)) * sizeof(double);
-  if (!st.host_stream) TB_CUDA(cudaStreamCreateWithFlags(&st.host_stream, cudaStreamNonBlocking), "stream create");
+  for (cudaStream_t* sp : {&st.host_stream, &st.h2d_stream, &st.d2h_stream})
+    if (!*sp) TB_CUDA(cudaStreamCreateWithFlags(sp, cudaStreamNonBlocking), "stream create");
   if (st.ws_bytes < need) {
     if (st.ws) cudaFree(st.ws);
     st.ws = nullptr;
@@ -504,41 +550,110 @@ int tb_gpu_tiled_multiply_flat_ex(int32_t device, const double* a, const double*
   double* dA = st.ws;
   double* dB = dA + up(na);
   double* dC = dB + up(nb);
-  cudaStream_t stream = st.host_stream;
-  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
-  int rc = TB_STATUS_OK;
-  for (auto& e : ev)
-    if (cudaEventCreate(&e) != cudaSuccess) rc = cuda_fail(cudaGetLastError(), "event create");
-  if (rc == TB_STATUS_OK) {
-    cudaEventRecord(ev[0], stream);
-    cudaError_t e = cudaMemcpyAsync(dA, a, na * sizeof(double), cudaMemcpyHostToDevice, stream);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(dB, b, nb * sizeof(double), cudaMemcpyHostToDevice, stream);
-    if (e != cudaSuccess) rc = cuda_fail(e, "host to device copy");
+  const cudaStream_t cs = st.host_stream, hs = st.h2d_stream, ds = st.d2h_stream;
+
+  // Copy/compute/copy pipeline over three streams (H2D, compute, D2H):
+  //  - R row blocks of A/C; P K-panels of B (contiguous row slices of B);
+  //  - the first Q row blocks are computed panel by panel as B's panels land
+  //    (C_r (+)= A_r[:, panel] · B[panel, :]), hiding B's transfer;
+  //  - later blocks run full-K while the next A block streams in and the
+  //    previous C block streams out.
+  // Small problems degenerate to one block / one panel (copy, GEMM, copy).
+  const double flops = 2.0 * (double)m * (double)n * (double)k;
+  int R = 1, P = 1;
+  if (flops >= 1e11) {
+    R = (int)std::min<int64_t>(8, std::max<int64_t>(1, m / 512));
+    P = (int)std::min<int64_t>(8, std::max<int64_t>(1, k / 256));
   }
-  if (rc == TB_STATUS_OK) {
-    cudaEventRecord(ev[1], stream);
-    rc = launch(device, dA, k, dB, n, dC, n, m, k, n, 0, tile_edge, variant, stream);
+  const int Q = std::max(1, (R + 3) / 4);
+  std::vector<int64_t> rb(R + 1), pb(P + 1);
+  for (int r = 0; r <= R; ++r) rb[r] = m * r / R;
+  for (int p = 0; p <= P; ++p) pb[p] = (k * p / P) & ~int64_t(1);  // even k0 keeps TMA 16-byte alignment
+  pb[P] = k;
+
+  std::vector<cudaEvent_t> evs;
+  auto mk = [&](unsigned flags) -> cudaEvent_t {
+    cudaEvent_t e = nullptr;
+    if (cudaEventCreateWithFlags(&e, flags) != cudaSuccess) return nullptr;
+    evs.push_back(e);
+    return e;
+  };
+  struct Cleanup {
+    std::vector<cudaEvent_t>& v;
+    ~Cleanup() {
+      for (auto e : v) cudaEventDestroy(e);
+    }
+  } cleanup{evs};
+  cudaEvent_t e_start = mk(cudaEventDefault), e_end = mk(cudaEventDefault);
+  std::vector<cudaEvent_t> evA(R), evB(P), evC(R), kt0, kt1;
+  for (auto& e : evA) e = mk(cudaEventDisableTiming);
+  for (auto& e : evB) e = mk(cudaEventDisableTiming);
+  for (auto& e : evC) e = mk(cudaEventDisableTiming);
+  for (auto e : evs)
+    if (!e) return cuda_fail(cudaGetLastError(), "event create");
+
+  auto h2d = [&](double* dst, const double* src, size_t elems, cudaEvent_t done) -> int {
+    TB_CUDA(cudaMemcpyAsync(dst, src, elems * sizeof(double), cudaMemcpyHostToDevice, hs), "host to device copy");
+    TB_CUDA(cudaEventRecord(done, hs), "event record");
+    return TB_STATUS_OK;
+  };
+  auto gemm = [&](int r, int64_t k0, int64_t k1, bool acc) -> int {
+    cudaEvent_t t0 = mk(cudaEventDefault), t1 = mk(cudaEventDefault);
+    if (!t0 || !t1) return cuda_fail(cudaGetLastError(), "event create");
+    kt0.push_back(t0);
+    kt1.push_back(t1);
+    const int64_t r0 = rb[r], rows = rb[r + 1] - rb[r];
+    TB_CUDA(cudaEventRecord(t0, cs), "event record");
+    int rc = launch(device, dA + r0 * k + k0, k, dB + k0 * n, n, dC + r0 * n, n, rows, k1 - k0, n, acc ? 1 : 0,
+                    tile_edge, variant, cs);
+    if (rc) return rc;
+    TB_CUDA(cudaEventRecord(t1, cs), "event record");
+    return TB_STATUS_OK;
+  };
+
+  TB_CUDA(cudaEventRecord(e_start, hs), "event record");
+  TB_CUDA(cudaStreamWaitEvent(cs, e_start, 0), "stream wait");
+  TB_CUDA(cudaStreamWaitEvent(ds, e_start, 0), "stream wait");
+  // H2D order: A blocks 0..Q-1, B panels, remaining A blocks.
+  for (int r = 0; r < Q; ++r)
+    if ((s = h2d(dA + rb[r] * k, a + rb[r] * k, (size_t)((rb[r + 1] - rb[r]) * k), evA[r]))) return s;
+  for (int p = 0; p < P; ++p)
+    if ((s = h2d(dB + pb[p] * n, b + pb[p] * n, (size_t)((pb[p + 1] - pb[p]) * n), evB[p]))) return s;
+  for (int r = Q; r < R; ++r)
+    if ((s = h2d(dA + rb[r] * k, a + rb[r] * k, (size_t)((rb[r + 1] - rb[r]) * k), evA[r]))) return s;
+  // Compute: leading blocks panel-major (as B arrives), then full-K blocks.
+  for (int r = 0; r < Q; ++r) TB_CUDA(cudaStreamWaitEvent(cs, evA[r], 0), "stream wait");
+  for (int p = 0; p < P; ++p) {
+    TB_CUDA(cudaStreamWaitEvent(cs, evB[p], 0), "stream wait");
+    for (int r = 0; r < Q; ++r)
+      if ((s = gemm(r, pb[p], pb[p + 1], p > 0))) return s;
   }
-  if (rc == TB_STATUS_OK) {
-    cudaEventRecord(ev[2], stream);
-    cudaError_t e = cudaMemcpyAsync(out_c, dC, nc * sizeof(double), cudaMemcpyDeviceToHost, stream);
-    if (e != cudaSuccess) rc = cuda_fail(e, "device to host copy");
+  for (int r = 0; r < R; ++r) {
+    if (r >= Q) {
+      TB_CUDA(cudaStreamWaitEvent(cs, evA[r], 0), "stream wait");
+      if ((s = gemm(r, 0, k, false))) return s;
+    }
+    TB_CUDA(cudaEventRecord(evC[r], cs), "event record");
+    // D2H of block r as soon as it is final.
+    TB_CUDA(cudaStreamWaitEvent(ds, evC[r], 0), "stream wait");
+    TB_CUDA(cudaMemcpyAsync(out_c + rb[r] * n, dC + rb[r] * n, (size_t)((rb[r + 1] - rb[r]) * n) * sizeof(double),
+                            cudaMemcpyDeviceToHost, ds),
+            "device to host copy");
   }
-  if (rc == TB_STATUS_OK) {
-    cudaEventRecord(ev[3], stream);
-    cudaError_t e = cudaEventSynchronize(ev[3]);
-    if (e != cudaSuccess) rc = cuda_fail(e, "kernel execution");
+  TB_CUDA(cudaEventRecord(e_end, ds), "event record");
+  TB_CUDA(cudaEventSynchronize(e_end), "kernel execution");
+  TB_CUDA(cudaStreamSynchronize(cs), "kernel execution");
+  double ksum = 0.0;
+  for (size_t i = 0; i < kt0.size(); ++i) {
+    float ms = 0.f;
+    TB_CUDA(cudaEventElapsedTime(&ms, kt0[i], kt1[i]), "event elapsed");
+    ksum += ms;
   }
-  if (rc == TB_STATUS_OK) {
-    float k_ms = 0.f, e_ms = 0.f;
-    cudaEventElapsedTime(&k_ms, ev[1], ev[2]);
-    cudaEventElapsedTime(&e_ms, ev[0], ev[3]);
-    *out_seconds = (double)k_ms * 1e-3;
-    if (out_e2e_seconds) *out_e2e_seconds = (double)e_ms * 1e-3;
-  }
-  for (auto& e : ev)
-    if (e) cudaEventDestroy(e);
-  return rc;
+  float e_ms = 0.f;
+  TB_CUDA(cudaEventElapsedTime(&e_ms, e_start, e_end), "event elapsed");
+  *out_seconds = ksum * 1e-3;  // kernel-only: sum of the GEMM launches
+  if (out_e2e_seconds) *out_e2e_seconds = (double)e_ms * 1e-3;
+  return TB_STATUS_OK;
 }
 
 int tb_gpu_tiled_multiply_flat(int32_t device, const double* a, const double* b, int64_t m, int64_t k, int64_t n,
@@ -559,8 +674,10 @@ void tb_release(void) {
     st.ws_bytes = 0;
     if (st.cublas) cublasDestroy(st.cublas);
     st.cublas = nullptr;
-    if (st.host_stream) cudaStreamDestroy(st.host_stream);
-    st.host_stream = nullptr;
+    for (cudaStream_t* sp : {&st.host_stream, &st.h2d_stream, &st.d2h_stream}) {
+      if (*sp) cudaStreamDestroy(*sp);
+      *sp = nullptr;
+    }
     for (auto& kv : st.split_ws) {
       if (kv.second.partials) cudaFree(kv.second.partials);
       if (kv.second.counters) cudaFree(kv.second.counters);

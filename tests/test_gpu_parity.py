@@ -265,3 +265,29 @@ def test_sharded_gemm_single_rank_nccl_panels(tb, oracle):
             assert oracle.normwise_rel(out.cpu().numpy(), ref) <= NORMWISE
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("m,k,n", [(4000, 4000, 4000), (3001, 2999, 2500)])
+def test_flat_pipelined_host_path(tb, golden, oracle, m, k, n):
+    """Large host-buffer calls run the 3-stream copy/compute pipeline (row
+    blocks x K-panels); results must match the single-launch device path."""
+    import torch
+
+    meta, g = golden
+    a, b = oracle.generate(m, k, 1), oracle.generate(k, n, 2)
+    a_h = torch.from_numpy(a).pin_memory()
+    b_h = torch.from_numpy(b).pin_memory()
+    c_h = torch.empty((m, n), dtype=torch.float64).pin_memory()
+    out_s, e2e = np.zeros(1), np.zeros(1)
+    assert tb.gpu_tiled_multiply_flat(0, a_h, b_h, m, k, n, 32, c_h, out_s, out_e2e_seconds=e2e) == tb.STATUS_OK
+    assert e2e[0] > 0 and out_s[0] > 0
+    ref, _ = tb.cublas_dgemm(a_h.cuda(), b_h.cuda())
+    got = c_h.cuda()
+    assert (torch.linalg.norm(got - ref) / torch.linalg.norm(ref)).item() <= NORMWISE
+    if (m, k, n) == (4000, 4000, 4000):
+        rows = g["n4000_rows"]
+        assert oracle.normwise_rel(c_h.numpy()[rows], g["n4000_tiled32_rows"]) <= NORMWISE
+    # pageable host buffers take the same path
+    c2 = np.zeros(m * n)
+    assert tb.gpu_tiled_multiply_flat(0, a, b, m, k, n, 32, c2, out_s) == tb.STATUS_OK
+    assert oracle.normwise_rel(c2.reshape(m, n), c_h.numpy()) <= NORMWISE

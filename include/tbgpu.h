@@ -59,7 +59,8 @@ extern "C" {
 #define TB_VARIANT_PAPER 1
 #define TB_VARIANT_DMMA_TMA 2
 #define TB_VARIANT_DMMA_CPASYNC 3
-#define TB_NUM_VARIANTS 4
+#define TB_VARIANT_DFMA 4 /* same pipeline/schedule, scalar DFMA 8x8 register tiles (comparison path) */
+#define TB_NUM_VARIANTS 5
 
 #define TB_DEFAULT_TILE_EDGE 32 /* limits.ts:40-42 */
 

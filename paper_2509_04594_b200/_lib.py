@@ -27,8 +27,9 @@ VARIANT_AUTO = 0
 VARIANT_PAPER = 1
 VARIANT_DMMA_TMA = 2
 VARIANT_DMMA_CPASYNC = 3
+VARIANT_DFMA = 4
 VARIANTS = {"auto": VARIANT_AUTO, "paper": VARIANT_PAPER, "dmma_tma": VARIANT_DMMA_TMA,
-            "dmma_cpasync": VARIANT_DMMA_CPASYNC}
+            "dmma_cpasync": VARIANT_DMMA_CPASYNC, "dfma": VARIANT_DFMA}
 
 DEFAULT_TILE_EDGE = 32
 

@@ -36,6 +36,9 @@
 namespace tb {
 
 enum class Loader : int { TMA = 0, CPASYNC = 1 };
+// Consumer arithmetic: DMMA (mma.sync m8n8k4 f64, warp-cooperative 8x8x4) or
+// DFMA (scalar fused multiply-add, 8x8 register tile per thread).
+enum class Math : int { DMMA = 0, DFMA = 1 };
 
 struct DmmaCfg {
   static constexpr int BM = 128, BN = 128, BK = 16;
@@ -126,7 +129,7 @@ struct WorkIter {
 
 __device__ __forceinline__ void consumer_bar() { asm volatile("bar.sync 1, %0;\n" ::"n"(DmmaCfg::CONSUMER_THREADS)); }
 
-template <int SUB, int STAGES, Loader LD>
+template <int SUB, int STAGES, Loader LD, Math MT = Math::DMMA>
 __global__ void __launch_bounds__(DmmaCfg::THREADS, 1)
     dgemm_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       const GemmParams p) {
@@ -227,6 +230,25 @@ __global__ void __launch_bounds__(DmmaCfg::THREADS, 1)
   const int cw = warp - 4;
   const int wm = cw / C::WARPS_N, wn = cw % C::WARPS_N;
   const int q = lane & 3, g = lane >> 2;
+  // Output coordinates of acc[i][j][e] inside the CTA tile:
+  //   row = row_base + i * row_step, col = col_base + j * col_step + e.
+  // DMMA: 2 x 4 warps of 64 x 32 (C fragment rows g, cols 2q).
+  // DFMA: 4 x 2 warps of 32 x 64; lane (lr, lc) = (lane >> 3, lane & 7) owns
+  //       rows lr + 4i and column pairs 2lc + 16j, so a quarter-warp shares
+  //       one A row (broadcast) and covers 8 distinct 16-byte B chunks.
+  const int lr = lane >> 3, lc = lane & 7;
+  const int row_base = MT == Math::DMMA ? wm * C::WM + g : (cw >> 1) * 32 + lr;
+  const int row_step = MT == Math::DMMA ? 8 : 4;
+  const int col_base = MT == Math::DMMA ? wn * C::WN + 2 * q : (cw & 1) * 64 + 2 * lc;
+  const int col_step = MT == Math::DMMA ? 8 : 16;
+  // DFMA A offsets: row ra = row_base + 4i, 16-byte chunk kp -> kp ^ (ra & 7),
+  // so byte = dfma_a[i] ^ (kp << 4) with dfma_a[i] = ra*128 + ((ra & 7) << 4).
+  uint32_t dfma_a[C::MI];
+#pragma unroll
+  for (int i = 0; i < C::MI; ++i) {
+    const int ra = row_base + 4 * i;
+    dfma_a[i] = ra * 128 + ((ra & 7) << 4);
+  }
   const int pa = 2 * q + (q >> 1);  // {0,2,5,7}
   const int pb = pa ^ 1;            // {1,3,4,6}
 
@@ -257,6 +279,40 @@ __global__ void __launch_bounds__(DmmaCfg::THREADS, 1)
 
     for (int kt = kb; kt < ke; ++kt) {
       mbar_wait(smem_u32(&full[s]), ph);
+      if constexpr (MT == Math::DFMA) {
+#pragma unroll
+        for (int u = 0; u < SUB; ++u) {
+          const uint8_t* sa = smem + s * STAGE_BYTES + u * C::STAGE;
+          const uint8_t* sb = sa + C::A_STAGE + (cw & 1) * 4 * C::B_BOX;
+#pragma unroll
+          for (int kp = 0; kp < C::BK / 2; ++kp) {
+            double2 a[C::MI], b0[C::NI], b1[C::NI];
+#pragma unroll
+            for (int i = 0; i < C::MI; ++i) a[i] = *reinterpret_cast<const double2*>(sa + (dfma_a[i] ^ (kp << 4)));
+            const uint32_t o0 = (2 * kp) * 128 + ((lc ^ ((2 * kp) & 7)) << 4);
+            const uint32_t o1 = (2 * kp + 1) * 128 + ((lc ^ ((2 * kp + 1) & 7)) << 4);
+#pragma unroll
+            for (int j = 0; j < C::NI; ++j) {
+              b0[j] = *reinterpret_cast<const double2*>(sb + j * C::B_BOX + o0);
+              b1[j] = *reinterpret_cast<const double2*>(sb + j * C::B_BOX + o1);
+            }
+#pragma unroll
+            for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+              for (int j = 0; j < C::NI; ++j) {
+                acc[i][j][0] = fma(a[i].x, b0[j].x, acc[i][j][0]);
+                acc[i][j][1] = fma(a[i].x, b0[j].y, acc[i][j][1]);
+              }
+#pragma unroll
+            for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+              for (int j = 0; j < C::NI; ++j) {
+                acc[i][j][0] = fma(a[i].y, b1[j].x, acc[i][j][0]);
+                acc[i][j][1] = fma(a[i].y, b1[j].y, acc[i][j][1]);
+              }
+          }
+        }
+      } else {
 #pragma unroll
       for (int hs = 0; hs < 2 * SUB; ++hs) {
         const int half = hs & 1;
@@ -281,6 +337,7 @@ __global__ void __launch_bounds__(DmmaCfg::THREADS, 1)
         for (int i = 0; i < C::MI; ++i)
 #pragma unroll
           for (int j = 0; j < C::NI; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i].y, bf[1][j]);
+      }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(&empty[s]));
@@ -336,12 +393,12 @@ __global__ void __launch_bounds__(DmmaCfg::THREADS, 1)
     const int m0 = tm * C::BM, n0 = tn * C::BN;
 #pragma unroll
     for (int i = 0; i < C::MI; ++i) {
-      const int r = m0 + wm * C::WM + i * 8 + g;
+      const int r = m0 + row_base + i * row_step;
       if (r >= p.m) continue;
       double* crow = p.C + (int64_t)r * p.ldc;
 #pragma unroll
       for (int j = 0; j < C::NI; ++j) {
-        const int c = n0 + wn * C::WN + j * 8 + 2 * q;
+        const int c = n0 + col_base + j * col_step;
         double v0 = acc[i][j][0], v1 = acc[i][j][1];
         if (c + 1 < p.n) {
           if (p.accumulate) {

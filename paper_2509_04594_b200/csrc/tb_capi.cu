@@ -48,10 +48,15 @@ template <int SUB, int STAGES>
 struct KernelSet {
   static void* tma() { return (void*)tb::dgemm_dmma_kernel<SUB, STAGES, tb::Loader::TMA>; }
   static void* cpasync() { return (void*)tb::dgemm_dmma_kernel<SUB, STAGES, tb::Loader::CPASYNC>; }
+  static void* dfma(bool tma) {
+    return tma ? (void*)tb::dgemm_dmma_kernel<SUB, STAGES, tb::Loader::TMA, tb::Math::DFMA>
+               : (void*)tb::dgemm_dmma_kernel<SUB, STAGES, tb::Loader::CPASYNC, tb::Math::DFMA>;
+  }
   static constexpr int smem() { return tb::dmma_smem_bytes<SUB, STAGES>(); }
 };
 
-void* cfg_kernel(int idx, bool tma) {
+void* cfg_kernel(int idx, bool tma, bool dfma = false) {
+  if (dfma) return KernelSet<1, 6>::dfma(tma);  // DFMA comparison variant: one pipeline shape
   switch (idx) {
     case 1: return tma ? KernelSet<1, 7>::tma() : KernelSet<1, 7>::cpasync();
     case 2: return tma ? KernelSet<2, 3>::tma() : KernelSet<2, 3>::cpasync();
@@ -153,6 +158,9 @@ int ensure_kernel_attrs(int dev) {
   DeviceState& st = g_dev[dev];
   std::lock_guard<std::mutex> lk(st.mu);
   if (st.attrs_set) return TB_STATUS_OK;
+  for (bool tma : {true, false})
+    TB_CUDA(cudaFuncSetAttribute(cfg_kernel(0, tma, true), cudaFuncAttributeMaxDynamicSharedMemorySize, cfg_smem(0)),
+            "set smem attribute (dfma)");
   for (int i = 0; i < kNumCfgs; ++i) {
     if (cfg_smem(i) > st.smem_optin) continue;  // validate() rejects the active one if it does not fit
     TB_CUDA(cudaFuncSetAttribute(cfg_kernel(i, true), cudaFuncAttributeMaxDynamicSharedMemorySize, cfg_smem(i)),
@@ -211,7 +219,7 @@ bool tma_ok(const void* A, int64_t lda, const void* B, int64_t ldb) {
 int resolve(const void* A, int64_t lda, const void* B, int64_t ldb, int variant) {
   if (variant == TB_VARIANT_AUTO) return tma_ok(A, lda, B, ldb) ? TB_VARIANT_DMMA_TMA : TB_VARIANT_DMMA_CPASYNC;
   if (variant == TB_VARIANT_DMMA_TMA && !tma_ok(A, lda, B, ldb)) return TB_VARIANT_DMMA_CPASYNC;
-  return variant;
+  return variant;  // DFMA picks its loader at launch (TMA when aligned)
 }
 
 // validateLaunch (limits.ts:58-79) plus this kernel family's own limits.
@@ -362,7 +370,8 @@ int launch(int dev, const double* A, int64_t lda, const double* B, int64_t ldb, 
       set_err("too many output tiles");
       return TB_STATUS_OVER_LIMITS;
     }
-    const int cfg = active_cfg();
+    const bool dfma = variant == TB_VARIANT_DFMA;
+    const int cfg = dfma ? 0 : active_cfg();
     const int64_t kstage = (int64_t)Cfg::BK * kCfgs[cfg].sub;
     p.num_k = (int)((k + kstage - 1) / kstage);
     const Schedule sc = plan_schedule(tiles, p.num_k, g_dev[dev].sms);
@@ -379,14 +388,14 @@ int launch(int dev, const double* A, int64_t lda, const double* B, int64_t ldb, 
     CUtensorMap mA, mB;
     std::memset(&mA, 0, sizeof(mA));
     std::memset(&mB, 0, sizeof(mB));
-    const bool use_tma = variant == TB_VARIANT_DMMA_TMA;
+    const bool use_tma = variant == TB_VARIANT_DMMA_TMA || (dfma && tma_ok(A, lda, B, ldb));
     if (use_tma) {
       if ((s = get_encoder())) return s;
       if ((s = encode_map(&mA, A, m, k, lda, Cfg::BM))) return s;
       if ((s = encode_map(&mB, B, k, n, ldb, Cfg::BK))) return s;
     }
     void* args[] = {&mA, &mB, &p};
-    TB_CUDA(cudaLaunchKernel(cfg_kernel(cfg, use_tma), dim3((unsigned)sc.grid), dim3(Cfg::THREADS), args,
+    TB_CUDA(cudaLaunchKernel(cfg_kernel(cfg, use_tma, dfma), dim3((unsigned)sc.grid), dim3(Cfg::THREADS), args,
                              (size_t)cfg_smem(cfg), stream),
             "kernel launch");
   }
@@ -472,6 +481,7 @@ const char* tb_variant_name(int32_t variant) {
     case TB_VARIANT_PAPER: return "paper";
     case TB_VARIANT_DMMA_TMA: return "dmma_tma";
     case TB_VARIANT_DMMA_CPASYNC: return "dmma_cpasync";
+    case TB_VARIANT_DFMA: return "dfma";
     default: return nullptr;
   }
 }

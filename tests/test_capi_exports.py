@@ -47,6 +47,7 @@ def test_kernels_use_dmma_and_tma():
 
     sass = subprocess.run(["cuobjdump", "-sass", _lib.LIB_PATH], capture_output=True, text=True).stdout
     assert "DMMA.8x8x4" in sass
+    assert "DFMA" in sass  # comparison variant
     assert "UTMALDG" in sass
     assert "LDGSTS" in sass  # cp.async variant
 
@@ -56,11 +57,12 @@ def test_metadata_calls_without_device():
 
     lib = _lib.lib()
     assert lib.tb_version().decode().startswith("tbgpu")
-    assert [lib.tb_variant_name(i).decode() for i in range(4)] == ["auto", "paper", "dmma_tma", "dmma_cpasync"]
+    assert [lib.tb_variant_name(i).decode() for i in range(5)] == ["auto", "paper", "dmma_tma", "dmma_cpasync", "dfma"]
     assert lib.tb_variant_name(99) is None
     assert lib.tb_resolve_variant(ctypes.c_void_p(4096), 10, ctypes.c_void_p(4096), 10, 0) == 2
     assert lib.tb_resolve_variant(ctypes.c_void_p(4096), 11, ctypes.c_void_p(4096), 10, 0) == 3
     assert lib.tb_resolve_variant(ctypes.c_void_p(4104), 10, ctypes.c_void_p(4096), 10, 2) == 3
+    assert lib.tb_resolve_variant(None, 10, None, 10, 4) == 4
     assert lib.tb_resolve_variant(None, 10, None, 10, 7) == -1
 
 

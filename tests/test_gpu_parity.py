@@ -18,7 +18,7 @@ pytestmark = pytest.mark.gpu
 
 NORMWISE = 1e-12
 ELEMWISE = 1e-10
-FAST = ["dmma_tma", "dmma_cpasync"]
+FAST = ["dmma_tma", "dmma_cpasync", "dfma"]
 
 
 @pytest.fixture(scope="module")
@@ -198,7 +198,7 @@ def test_flat_abi_status_codes(tb, oracle):
     assert tb.gpu_tiled_multiply_flat(0, a, b, n, n, n, 4, np.zeros(3), out_s) == tb.STATUS_BAD_DIMS
     assert tb.gpu_tiled_multiply_flat(0, a, b, n, n, n, 0, out_c, out_s) == tb.STATUS_BAD_DIMS
     assert tb.gpu_tiled_multiply_flat(0, a, b, 0, n, n, 32, out_c, out_s) == tb.STATUS_BAD_DIMS
-    for v in ("paper", "dmma_tma", "dmma_cpasync"):
+    for v in ("paper", "dmma_tma", "dmma_cpasync", "dfma"):
         out_c[:] = 0
         e2e = np.zeros(1)
         assert tb.gpu_tiled_multiply_flat(0, a, b, n, n, n, 16, out_c, out_s, variant=v,

@@ -6,7 +6,7 @@ N = 10000, with % of B200 FP64 peak. One step = one C = A·B over the whole
 N x N problem (at N GPUs: B broadcast from rank 0 over NCCL + each rank's
 row-block GEMM).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--n 10000] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--size 10000] [--impl ours|reference]
 
 Prints ONE JSON line on rank 0. Inputs (800 MB per matrix at N = 10000) are
 larger than the 126 MB L2, so no flush is needed between steps.
@@ -124,25 +124,36 @@ class ClockSampler:
                 "samples": len(rows), "power_w_max": max(power) if power else None}
 
 
-def cpu_sample(n: int, threads: int, target_s: float, seed_a: int = 1, seed_b: int = 2) -> dict:
+def _cpu_operands(n: int, rows: int):
+    import numpy as np
+
+    b = np.random.Generator(np.random.PCG64(1)).random((n, n)) * 3.0 + 2.0
+    a = np.random.Generator(np.random.PCG64(2)).random((rows, n)) * 3.0 + 2.0
+    return a, b
+
+
+def cpu_calibrate(n: int, threads: int, target_s: float) -> int:
+    """Rows of the N x N product that take about target_s on the host cores."""
+    from oracle import oracle as ref
+
+    rows = max(threads, 16)
+    a, b = _cpu_operands(n, rows)
+    t0 = time.perf_counter()
+    ref.tiled_parallel(a, b, 32, threads)
+    dt = time.perf_counter() - t0
+    return int(min(n, max(threads, rows * target_s / max(dt, 1e-3))))
+
+
+def cpu_sample(n: int, threads: int, rows: int) -> dict:
     """The reference's CPU tiled path (oracle C port of tile_range_kernel +
     plan_partitions, pthreads) timed on a bounded row sample of the N x N
     workload; rows of tiled(A[rows], B) are bitwise rows of the full product."""
-    import numpy as np
-
     from oracle import oracle as ref
 
-    rng = np.random.Generator(np.random.PCG64(seed_a))
-    b = rng.random((n, n)) * 3.0 + 2.0
-    rows = 16
-    while True:
-        a = np.random.Generator(np.random.PCG64(seed_b)).random((rows, n)) * 3.0 + 2.0
-        t0 = time.perf_counter()
-        ref.tiled_parallel(a, b, 32, threads)
-        dt = time.perf_counter() - t0
-        if dt >= target_s or rows >= n:
-            break
-        rows = min(n, max(rows * 2, int(rows * target_s / max(dt, 1e-3) * 1.05)))
+    a, b = _cpu_operands(n, rows)
+    t0 = time.perf_counter()
+    ref.tiled_parallel(a, b, 32, threads)
+    dt = time.perf_counter() - t0
     flops = rows * (2 * n * n - n)
     return {"value": flops / dt / 1e9, "unit": UNIT, "cores": threads, "kind": "port",
             "sample": f"tiled-parallel K=32 (oracle/tb_oracle.c port of kernels.py:32-53 + backends.py:119-160) "
@@ -156,8 +167,9 @@ def run_reference(args) -> None:
         return
     threads = os.cpu_count() or 1
     vals = []
+    rows = cpu_calibrate(args.n, threads, args.ref_seconds)
     for i in range(args.warmup + args.steps):
-        s = cpu_sample(args.n, threads, target_s=args.ref_seconds)
+        s = cpu_sample(args.n, threads, rows)
         if i >= args.warmup:
             vals.append(s)
     v = statistics.median([s["value"] for s in vals])
@@ -183,10 +195,16 @@ def run_ours(args) -> None:
     rank, world, local = env_rank()
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}; launch N>1 under torchrun")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # TB_BENCH_SHARED_DEVICE=1 puts every rank on cuda:0 (exercises the N>1
+    # code path on a 1-GPU box with --dist-backend gloo; not a measurement).
+    local_dev = 0 if os.environ.get("TB_BENCH_SHARED_DEVICE") == "1" else local
+    torch.cuda.set_device(local_dev)
+    dev = torch.device("cuda", local_dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(args.dist_backend)
     n = args.n
     parts = row_partitions(n, world)
     r0, r1 = parts[rank]
@@ -217,7 +235,7 @@ def run_ours(args) -> None:
     barrier()
     # kernel-only launch timing of the dominant kernel on its own stream (roofline achieved)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * args.steps)]
-    with ClockSampler(local) as clocks:
+    with ClockSampler(local_dev) as clocks:
         barrier()
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
@@ -292,7 +310,7 @@ def run_ours(args) -> None:
     for i in range(1 + max(2, args.steps // 3)):
         if world > 1:
             dist.barrier()
-        st = tb.gpu_tiled_multiply_flat(local, a_h, b_h, r1 - r0, n, n, 32, c_h, out_s,
+        st = tb.gpu_tiled_multiply_flat(local_dev, a_h, b_h, r1 - r0, n, n, 32, c_h, out_s,
                                         variant=args.variant, out_e2e_seconds=e2e)
         if st != 0:
             raise RuntimeError(f"flat ABI status {st}: {_lib.last_error()}")
@@ -309,7 +327,8 @@ def run_ours(args) -> None:
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_sample(n, os.cpu_count() or 1, target_s=args.ref_seconds)
+        threads = os.cpu_count() or 1
+        cpu = cpu_sample(n, threads, cpu_calibrate(n, threads, args.ref_seconds))
         cpu.pop("seconds", None)
 
     if rank == 0:
@@ -351,12 +370,13 @@ def main():
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
-    p.add_argument("--n", type=int, default=10000)
+    p.add_argument("--size", dest="n", type=int, default=10000, help="matrix order N")
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--variant", default="auto")
     p.add_argument("--panels", type=int, default=4, help="K-panels of the B broadcast at N>1")
-    p.add_argument("--ref-seconds", type=float, default=10.0, help="CPU sample length per measurement")
+    p.add_argument("--ref-seconds", type=float, default=10.0, help="CPU sample length per measurement (s)")
     p.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    p.add_argument("--dist-backend", default="nccl", help="torch.distributed backend at N>1 (nccl; gloo for tests)")
     args = p.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3

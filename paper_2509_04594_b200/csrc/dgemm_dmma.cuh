@@ -166,6 +166,13 @@ __global__ void __launch_bounds__(DmmaCfg::THREADS, 1)
     }
     int s = 0;
     uint32_t ph = 0;
+    // cp.async loader: stage g's copies are committed as one group and its
+    // full barrier is arrived on (release) once cp.async.wait_group shows the
+    // group complete, CP_LAG stages later, so CP_LAG + 1 stages stay in
+    // flight. CP_LAG <= STAGES - 1 keeps every arrive ahead of the empty-slot
+    // wait that could depend on it (no deadlock).
+    constexpr int CP_LAG = STAGES - 1 < 4 ? STAGES - 1 : 4;
+    int g = 0;
     WorkIter w(p);
     int tile, kb, ke;
     while (w.next(p, tile, kb, ke)) {
@@ -193,33 +200,42 @@ __global__ void __launch_bounds__(DmmaCfg::THREADS, 1)
           const int pt = threadIdx.x;  // 0..127
 #pragma unroll
           for (int u = 0; u < SUB; ++u) {
-          const uint32_t sa = stage + u * C::STAGE, sb = sa + C::A_STAGE;
-          const int k0 = (kt * SUB + u) * C::BK;
+            const uint32_t sa = stage + u * C::STAGE, sb = sa + C::A_STAGE;
+            const int k0 = (kt * SUB + u) * C::BK;
 #pragma unroll 4
-          for (int i = 0; i < (C::BM * C::BK) / 128; ++i) {
-            const int e = i * 128 + pt, r = e >> 4, kk = e & 15;
-            const int gm = m0 + r, gk = k0 + kk;
-            const bool ok = gm < p.m && gk < p.k;
-            const double* src = ok ? p.A + (int64_t)gm * p.lda + gk : p.A;
-            cp_async_8(sa + r * 128 + (((kk >> 1) ^ (r & 7)) << 4) + (kk & 1) * 8, src, ok);
-          }
+            for (int i = 0; i < (C::BM * C::BK) / 128; ++i) {
+              const int e = i * 128 + pt, r = e >> 4, kk = e & 15;
+              const int gm = m0 + r, gk = k0 + kk;
+              const bool ok = gm < p.m && gk < p.k;
+              const double* src = ok ? p.A + (int64_t)gm * p.lda + gk : p.A;
+              cp_async_8(sa + r * 128 + (((kk >> 1) ^ (r & 7)) << 4) + (kk & 1) * 8, src, ok);
+            }
 #pragma unroll 4
-          for (int i = 0; i < (C::BK * C::BN) / 128; ++i) {
-            const int e = i * 128 + pt, kr = e >> 7, nn = e & 127;
-            const int gk = k0 + kr, gn = n0 + nn;
-            const bool ok = gk < p.k && gn < p.n;
-            const double* src = ok ? p.B + (int64_t)gk * p.ldb + gn : p.B;
-            cp_async_8(sb + (nn >> 4) * C::B_BOX + kr * 128 + ((((nn & 15) >> 1) ^ (kr & 7)) << 4) + (nn & 1) * 8,
-                       src, ok);
+            for (int i = 0; i < (C::BK * C::BN) / 128; ++i) {
+              const int e = i * 128 + pt, kr = e >> 7, nn = e & 127;
+              const int gk = k0 + kr, gn = n0 + nn;
+              const bool ok = gk < p.k && gn < p.n;
+              const double* src = ok ? p.B + (int64_t)gk * p.ldb + gn : p.B;
+              cp_async_8(sb + (nn >> 4) * C::B_BOX + kr * 128 + ((((nn & 15) >> 1) ^ (kr & 7)) << 4) + (nn & 1) * 8,
+                         src, ok);
+            }
           }
+          cp_async_commit();
+          if (g >= CP_LAG) {
+            cp_async_wait<CP_LAG>();
+            mbar_arrive(smem_u32(&full[(g - CP_LAG) % STAGES]));
           }
-          cp_async_mbar_arrive_noinc(smem_u32(&full[s]));
+          ++g;
         }
         if (++s == STAGES) {
           s = 0;
           ph ^= 1;
         }
       }
+    }
+    if constexpr (LD == Loader::CPASYNC) {
+      cp_async_wait<0>();
+      for (int x = g > CP_LAG ? g - CP_LAG : 0; x < g; ++x) mbar_arrive(smem_u32(&full[x % STAGES]));
     }
     return;
   }

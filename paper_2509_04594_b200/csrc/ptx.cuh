@@ -70,10 +70,12 @@ __device__ __forceinline__ void cp_async_8(uint32_t dst, const void* src, bool v
                : "memory");
 }
 
-// Make the mbarrier track completion of this thread's prior cp.async ops
-// (does not increment the pending count: the barrier's init count includes it).
-__device__ __forceinline__ void cp_async_mbar_arrive_noinc(uint32_t bar) {
-  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(bar) : "memory");
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+
+// Wait until at most N of this thread's committed cp.async groups are pending.
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
 // ---- warpgroup register reallocation (all 128 threads of a warpgroup) ----

@@ -1,0 +1,64 @@
+// Small C-ABI driver for compute-sanitizer (memcheck / racecheck / synccheck):
+// runs every variant on ragged shapes that exercise TMA out-of-bounds fill,
+// the cp.async zero-fill path, the stream-K split/fixup path and the paper
+// kernel, through include/tbgpu.h only. Exit code 0 = all calls OK.
+//   nvcc -O2 -I include -o tools/sanitize_driver tools/sanitize_driver.cu \
+//        -L paper_2509_04594_b200 -ltbgpu -Xlinker -rpath,$PWD/paper_2509_04594_b200
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "tbgpu.h"
+
+// Usage: sanitize_driver [--tma-only]
+//   --tma-only: even shapes and TMA-fed variants only (racecheck does not
+//   model mbarrier-ordered cp.async writes; see tests/test_gpu_sanitizer.py).
+int main(int argc, char** argv) {
+  const bool tma_only = argc > 1 && std::string(argv[1]) == "--tma-only";
+  struct Shape {
+    long m, k, n;
+  };
+  const Shape shapes[] = {{33, 33, 33}, {129, 130, 131}, {256, 300, 128}, {515, 515, 515}, {130, 66, 258}};
+  std::vector<int> variants = {TB_VARIANT_PAPER, TB_VARIANT_DMMA_TMA, TB_VARIANT_DFMA};
+  if (!tma_only) variants.push_back(TB_VARIANT_DMMA_CPASYNC);
+  int failures = 0;
+  for (const Shape& s : shapes) {
+    if (tma_only && (s.k % 2 || s.n % 2)) continue;
+    std::vector<double> a(s.m * s.k), b(s.k * s.n), ref(s.m * s.n, 0.0), c(s.m * s.n);
+    for (size_t i = 0; i < a.size(); ++i) a[i] = 2.0 + 3.0 * ((i * 2654435761u) % 1000) / 1000.0;
+    for (size_t i = 0; i < b.size(); ++i) b[i] = 2.0 + 3.0 * ((i * 40503u) % 1000) / 1000.0;
+    for (long i = 0; i < s.m; ++i)
+      for (long p = 0; p < s.k; ++p)
+        for (long j = 0; j < s.n; ++j) ref[i * s.n + j] += a[i * s.k + p] * b[p * s.n + j];
+    double *dA, *dB, *dC;
+    cudaMalloc(&dA, a.size() * 8);
+    cudaMalloc(&dB, b.size() * 8);
+    cudaMalloc(&dC, c.size() * 8);
+    cudaMemcpy(dA, a.data(), a.size() * 8, cudaMemcpyHostToDevice);
+    cudaMemcpy(dB, b.data(), b.size() * 8, cudaMemcpyHostToDevice);
+    for (int v : variants) {
+      double sec = 0;
+      const int st = tb_dgemm(dA, dB, dC, s.m, s.k, s.n, 32, v, 0, nullptr, &sec);
+      cudaMemcpy(c.data(), dC, c.size() * 8, cudaMemcpyDeviceToHost);
+      double num = 0, den = 0;
+      for (size_t i = 0; i < c.size(); ++i) {
+        num += (c[i] - ref[i]) * (c[i] - ref[i]);
+        den += ref[i] * ref[i];
+      }
+      const double rel = std::sqrt(num / den);
+      const bool ok = st == TB_STATUS_OK && rel <= 1e-12;
+      failures += !ok;
+      std::printf("%ldx%ldx%ld variant=%s status=%d normwise=%.2e %s\n", s.m, s.k, s.n, tb_variant_name(v), st, rel,
+                  ok ? "ok" : tb_last_error());
+    }
+    cudaFree(dA);
+    cudaFree(dB);
+    cudaFree(dC);
+  }
+  tb_release();
+  return failures ? 1 : 0;
+}

@@ -291,3 +291,14 @@ def test_flat_pipelined_host_path(tb, golden, oracle, m, k, n):
     c2 = np.zeros(m * n)
     assert tb.gpu_tiled_multiply_flat(0, a, b, m, k, n, 32, c2, out_s) == tb.STATUS_OK
     assert oracle.normwise_rel(c2.reshape(m, n), c_h.numpy()) <= NORMWISE
+
+
+def test_cli_run_writes_reference_csv(tb, tmp_path):
+    from paper_2509_04594_b200.__main__ import main
+
+    out = tmp_path / "gpu.csv"
+    assert main(["run", "--backends", "gpu-tiled,cublas-dgemm", "--sizes", "64,200", "--trials", "2",
+                 "--verify", "--out", str(out)]) == 0
+    lines = out.read_text().splitlines()
+    assert lines[0] == "backend,n,trial,seconds,flops" and len(lines) == 1 + 2 * 2 * 2
+    assert (tmp_path / "gpu.csv.meta.json").exists()

@@ -169,3 +169,46 @@ def test_gpu_entry_points_refuse_cpu_tensors():
 
     with pytest.raises(tb.ShapeError):
         tb.dgemm(torch.ones(2, 2, dtype=torch.float64), torch.ones(2, 2, dtype=torch.float64))
+
+
+def test_cli_bad_config_exit_code(tmp_path, monkeypatch):
+    """cli.py:110-115: unknown backend -> exit 2 before any trial."""
+    from paper_2509_04594_b200.__main__ import main
+
+    monkeypatch.setattr(tb.backends, "probe_device", lambda: None)
+    assert main(["run", "--backends", "nope", "--sizes", "8", "--out", str(tmp_path / "x.csv")]) == 2
+    assert not (tmp_path / "x.csv").exists()
+
+
+REF_SRC = "/root/reference/pkg/src"
+
+
+@pytest.mark.skipif(not __import__("os").path.isdir(REF_SRC), reason="reference tree not present (GPU box)")
+def test_records_readable_by_reference_reader(tmp_path):
+    """Our CSV + sidecar round-trip through the reference's own read_records
+    (records.py:76-112), imported from a temp copy (numba cache stays out of
+    /root/reference)."""
+    import importlib
+    import os
+    import shutil
+    import sys
+
+    copy = tmp_path / "ref"
+    shutil.copytree(REF_SRC, copy / "src")
+    os.environ["NUMBA_CACHE_DIR"] = str(tmp_path / "nc")
+    sys.path.insert(0, str(copy / "src"))
+    try:
+        records_mod = importlib.import_module("tilebench.records")
+        recs = [tb.TrialRecord("gpu-tiled", 1000, t, 5.6e-5 * (1 + t), tb.flop_count(1000) / (5.6e-5 * (1 + t)))
+                for t in range(3)]
+        meta = tb.RunMetadata.capture(tb.RunConfig(backends=("gpu-tiled",), sizes=(1000,), trials=3))
+        p = tmp_path / "gpu.csv"
+        tb.write_records(p, recs, meta)
+        back, m = records_mod.read_records(p)
+        assert [(r.backend, r.n, r.trial, r.seconds, r.flops) for r in back] == \
+            [(r.backend, r.n, r.trial, r.seconds, r.flops) for r in recs]
+        assert m.cores == meta.cores
+    finally:
+        sys.path.remove(str(copy / "src"))
+        for k in [k for k in sys.modules if k == "tilebench" or k.startswith("tilebench.")]:
+            del sys.modules[k]

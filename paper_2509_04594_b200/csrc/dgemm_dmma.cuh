@@ -103,11 +103,12 @@ __device__ __forceinline__ void tile_coords(int tile, int tiles_m, int tiles_n, 
 // The CTA's static work list: (tile, [kb, ke)) units. Producer and consumers
 // each walk their own copy, so they agree without communicating.
 struct WorkIter {
-  int t, it, end;
+  int t;
+  int64_t it, end;  // stream-K iteration range (64-bit: sk_tiles * num_k may exceed 2^31)
   __device__ __forceinline__ explicit WorkIter(const GemmParams& p) {
     t = blockIdx.x;
-    it = blockIdx.x * p.sk_ipc;
-    end = min(it + p.sk_ipc, p.sk_tiles * p.num_k);
+    it = (int64_t)blockIdx.x * p.sk_ipc;
+    end = min(it + p.sk_ipc, (int64_t)p.sk_tiles * p.num_k);
   }
   __device__ __forceinline__ bool next(const GemmParams& p, int& tile, int& kb, int& ke) {
     if (t < p.dp_tiles) {
@@ -118,9 +119,9 @@ struct WorkIter {
       return true;
     }
     if (it >= end) return false;
-    const int st = it / p.num_k;
-    kb = it - st * p.num_k;
-    ke = min(p.num_k, kb + (end - it));
+    const int st = (int)(it / p.num_k);
+    kb = (int)(it - (int64_t)st * p.num_k);
+    ke = (int)min((int64_t)p.num_k, kb + (end - it));
     tile = p.dp_tiles + st;
     it += ke - kb;
     return true;
@@ -366,9 +367,9 @@ __global__ void __launch_bounds__(DmmaCfg::THREADS, 1)
     // ------------------------------------------------- stream-K segment fixup
     if (kb != 0 || ke != p.num_k) {
       const int st = tile - p.dp_tiles;
-      const int first = st * p.num_k;
-      const int seg = (first + kb) / p.sk_ipc - first / p.sk_ipc;
-      const int nseg = (first + p.num_k - 1) / p.sk_ipc - first / p.sk_ipc + 1;
+      const int64_t first = (int64_t)st * p.num_k;
+      const int seg = (int)((first + kb) / p.sk_ipc - first / p.sk_ipc);
+      const int nseg = (int)((first + p.num_k - 1) / p.sk_ipc - first / p.sk_ipc + 1);
       double2* slots = reinterpret_cast<double2*>(p.partials) + (size_t)st * p.max_seg * (C::TILE_ELEMS / 2);
       double2* mine = slots + (size_t)seg * (C::TILE_ELEMS / 2);
 #pragma unroll

@@ -575,7 +575,16 @@ int tb_gpu_tiled_multiply_flat_ex(int32_t device, const double* a, const double*
     R = (int)std::min<int64_t>(8, std::max<int64_t>(1, m / 512));
     P = (int)std::min<int64_t>(8, std::max<int64_t>(1, k / 256));
   }
-  const int Q = std::max(1, (R + 3) / 4);
+  int Q = std::max(1, (R + 3) / 4);
+  // TB_PIPE=R,P,Q overrides the pipeline shape (tuning experiments).
+  if (const char* e = std::getenv("TB_PIPE")) {
+    int r = 0, pp = 0, qq = 0;
+    if (std::sscanf(e, "%d,%d,%d", &r, &pp, &qq) == 3 && r >= 1 && pp >= 1 && qq >= 1) {
+      R = (int)std::min<int64_t>(r, m);
+      P = (int)std::min<int64_t>(pp, std::max<int64_t>(1, k / 2));
+      Q = std::min(qq, R);
+    }
+  }
   std::vector<int64_t> rb(R + 1), pb(P + 1);
   for (int r = 0; r <= R; ++r) rb[r] = m * r / R;
   for (int p = 0; p <= P; ++p) pb[p] = (k * p / P) & ~int64_t(1);  // even k0 keeps TMA 16-byte alignment

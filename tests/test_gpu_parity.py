@@ -302,3 +302,33 @@ def test_cli_run_writes_reference_csv(tb, tmp_path):
     lines = out.read_text().splitlines()
     assert lines[0] == "backend,n,trial,seconds,flops" and len(lines) == 1 + 2 * 2 * 2
     assert (tmp_path / "gpu.csv.meta.json").exists()
+
+
+def test_n32768_sampled_exact_oracle(tb, oracle):
+    """configs[4] size (8.6 GB per matrix) on one B200: C[rows][:, cols] vs
+    the reference's tiled product on the same rows and columns
+    (tiled(A[rows], B[:, cols]) is entrywise bitwise equal to the full tiled
+    product: the k0 phases depend on k only), plus a full-matrix normwise
+    check of a row block against cuBLAS."""
+    import torch
+
+    n = 32768
+    g = torch.Generator(device="cuda").manual_seed(32768)
+    A = torch.rand((n, n), dtype=torch.float64, device="cuda", generator=g).mul_(3.0).add_(2.0)
+    B = torch.rand((n, n), dtype=torch.float64, device="cuda", generator=g).mul_(3.0).add_(2.0)
+    C, sec = tb.dgemm(A, B)
+    assert tb.flop_count(n) / sec / 1e12 > 20.0  # sanity: full-size run is on the fast path
+    rows = torch.tensor([0, 127, 128, 16383, 16384, 32639, 32640, 32767], device="cuda")
+    cols = torch.tensor(list(range(0, 16)) + list(range(16376, 16392)) + list(range(32752, 32768)), device="cuda")
+    a_rows = A[rows].cpu().numpy()
+    b_cols = B[:, cols].contiguous().cpu().numpy()
+    want = oracle.tiled_parallel(a_rows, b_cols)
+    got = C[rows][:, cols].cpu().numpy()
+    assert oracle.normwise_rel(got, want) <= NORMWISE
+    assert oracle.max_abs_rel_diff(got, want) <= ELEMWISE
+    # A 1024-row block of the full product against cuBLAS (keeps memory bounded).
+    ref, _ = tb.cublas_dgemm(A[8192:9216].contiguous(), B)
+    rel = (torch.linalg.norm(C[8192:9216] - ref) / torch.linalg.norm(ref)).item()
+    assert rel <= NORMWISE
+    del A, B, C, ref
+    torch.cuda.empty_cache()

@@ -102,7 +102,8 @@ struct DeviceState {
   int smem_optin = 0;
   bool attrs_set = false;
   cublasHandle_t cublas = nullptr;
-  cudaStream_t host_stream = nullptr;  // host-buffer entry: compute stream
+  cudaStream_t host_stream = nullptr;  // host-buffer entry: compute streams (even / odd row blocks)
+  cudaStream_t host_stream2 = nullptr;
   cudaStream_t h2d_stream = nullptr;   // host-buffer entry: host-to-device copies
   cudaStream_t d2h_stream = nullptr;   // host-buffer entry: device-to-host copies
   double* ws = nullptr;                // host-entry device workspace (A | B | C)
@@ -548,7 +549,7 @@ int tb_gpu_tiled_multiply_flat_ex(int32_t device, const double* a, const double*
   const size_t na = (size_t)(m * k), nb = (size_t)(k * n), nc = (size_t)(m * n);
   auto up = [](size_t x) { return (x + 31) & ~size_t(31); };  // 256-byte aligned sub-buffers
   const size_t need = (up(na) + up(nb) + up(nc)) * sizeof(double);
-  for (cudaStream_t* sp : {&st.host_stream, &st.h2d_stream, &st.d2h_stream})
+  for (cudaStream_t* sp : {&st.host_stream, &st.host_stream2, &st.h2d_stream, &st.d2h_stream})
     if (!*sp) TB_CUDA(cudaStreamCreateWithFlags(sp, cudaStreamNonBlocking), "stream create");
   if (st.ws_bytes < need) {
     if (st.ws) cudaFree(st.ws);
@@ -560,7 +561,11 @@ int tb_gpu_tiled_multiply_flat_ex(int32_t device, const double* a, const double*
   double* dA = st.ws;
   double* dB = dA + up(na);
   double* dC = dB + up(nb);
-  const cudaStream_t cs = st.host_stream, hs = st.h2d_stream, ds = st.d2h_stream;
+  const cudaStream_t hs = st.h2d_stream, ds = st.d2h_stream;
+  // Row blocks alternate between two compute streams so one launch's tail
+  // overlaps the next launch's head (blocks are independent).
+  const cudaStream_t css[2] = {st.host_stream, st.host_stream2};
+  auto cs_of = [&](int r) { return css[r & 1]; };
 
   // Copy/compute/copy pipeline over three streams (H2D, compute, D2H):
   //  - R row blocks of A/C; P K-panels of B (contiguous row slices of B);
@@ -622,6 +627,7 @@ int tb_gpu_tiled_multiply_flat_ex(int32_t device, const double* a, const double*
     kt0.push_back(t0);
     kt1.push_back(t1);
     const int64_t r0 = rb[r], rows = rb[r + 1] - rb[r];
+    const cudaStream_t cs = cs_of(r);
     TB_CUDA(cudaEventRecord(t0, cs), "event record");
     int rc = launch(device, dA + r0 * k + k0, k, dB + k0 * n, n, dC + r0 * n, n, rows, k1 - k0, n, acc ? 1 : 0,
                     tile_edge, variant, cs);
@@ -631,37 +637,75 @@ int tb_gpu_tiled_multiply_flat_ex(int32_t device, const double* a, const double*
   };
 
   TB_CUDA(cudaEventRecord(e_start, hs), "event record");
-  TB_CUDA(cudaStreamWaitEvent(cs, e_start, 0), "stream wait");
+  for (cudaStream_t cs : css) TB_CUDA(cudaStreamWaitEvent(cs, e_start, 0), "stream wait");
   TB_CUDA(cudaStreamWaitEvent(ds, e_start, 0), "stream wait");
-  // H2D order: A blocks 0..Q-1, B panels, remaining A blocks.
-  for (int r = 0; r < Q; ++r)
-    if ((s = h2d(dA + rb[r] * k, a + rb[r] * k, (size_t)((rb[r + 1] - rb[r]) * k), evA[r]))) return s;
-  for (int p = 0; p < P; ++p)
-    if ((s = h2d(dB + pb[p] * n, b + pb[p] * n, (size_t)((pb[p + 1] - pb[p]) * n), evB[p]))) return s;
-  for (int r = Q; r < R; ++r)
-    if ((s = h2d(dA + rb[r] * k, a + rb[r] * k, (size_t)((rb[r + 1] - rb[r]) * k), evA[r]))) return s;
-  // Compute: leading blocks panel-major (as B arrives), then full-K blocks.
-  for (int r = 0; r < Q; ++r) TB_CUDA(cudaStreamWaitEvent(cs, evA[r], 0), "stream wait");
-  for (int p = 0; p < P; ++p) {
-    TB_CUDA(cudaStreamWaitEvent(cs, evB[p], 0), "stream wait");
-    for (int r = 0; r < Q; ++r)
-      if ((s = gemm(r, pb[p], pb[p + 1], p > 0))) return s;
+  // H2D order: A0 B0 A1 B1 ... A(Q-1) B(Q-1), then the remaining B panels,
+  // then the remaining A blocks — the first compute cell (A0 x B0) is ready
+  // after two chunks and panel work grows as the transfers interleave.
+  struct Xfer {
+    bool is_a;
+    int idx;
+  };
+  std::vector<Xfer> order;
+  for (int i = 0; i < std::max(Q, P); ++i) {
+    if (i < Q) order.push_back({true, i});
+    if (i < P) order.push_back({false, i});
   }
-  for (int r = 0; r < R; ++r) {
-    if (r >= Q) {
-      TB_CUDA(cudaStreamWaitEvent(cs, evA[r], 0), "stream wait");
+  for (int r = Q; r < R; ++r) order.push_back({true, r});
+  std::vector<double> readyA(R), readyB(P);  // estimated arrival (bytes transferred so far)
+  double bytes = 0;
+  for (const Xfer& x : order) {
+    if (x.is_a) {
+      const int r = x.idx;
+      if ((s = h2d(dA + rb[r] * k, a + rb[r] * k, (size_t)((rb[r + 1] - rb[r]) * k), evA[r]))) return s;
+      bytes += (double)(rb[r + 1] - rb[r]) * k;
+      readyA[r] = bytes;
+    } else {
+      const int p = x.idx;
+      if ((s = h2d(dB + pb[p] * n, b + pb[p] * n, (size_t)((pb[p + 1] - pb[p]) * n), evB[p]))) return s;
+      bytes += (double)(pb[p + 1] - pb[p]) * n;
+      readyB[p] = bytes;
+    }
+  }
+  // Compute cells in estimated data-ready order: (r, p) panel cells for the
+  // first Q row blocks, then full-K blocks. A row's cells share a stream, so
+  // its partial sums accumulate in enqueue order (first cell overwrites C).
+  struct Cell {
+    double ready;
+    int r, p;  // p < 0: full-K block
+  };
+  std::vector<Cell> cells;
+  for (int r = 0; r < Q; ++r)
+    for (int p = 0; p < P; ++p) cells.push_back({std::max(readyA[r], readyB[p]), r, p});
+  for (int r = Q; r < R; ++r) cells.push_back({std::max(readyA[r], readyB[P - 1]), r, -1});
+  std::stable_sort(cells.begin(), cells.end(), [](const Cell& x, const Cell& y) { return x.ready < y.ready; });
+  std::vector<int> remaining(R);
+  for (int r = 0; r < R; ++r) remaining[r] = r < Q ? P : 1;
+  std::vector<bool> started(R, false);
+  for (const Cell& cl : cells) {
+    const int r = cl.r;
+    const cudaStream_t cs = cs_of(r);
+    TB_CUDA(cudaStreamWaitEvent(cs, evA[r], 0), "stream wait");
+    if (cl.p >= 0) {
+      TB_CUDA(cudaStreamWaitEvent(cs, evB[cl.p], 0), "stream wait");
+      if ((s = gemm(r, pb[cl.p], pb[cl.p + 1], started[r]))) return s;
+    } else {
+      for (int p = 0; p < P; ++p) TB_CUDA(cudaStreamWaitEvent(cs, evB[p], 0), "stream wait");
       if ((s = gemm(r, 0, k, false))) return s;
     }
-    TB_CUDA(cudaEventRecord(evC[r], cs), "event record");
-    // D2H of block r as soon as it is final.
-    TB_CUDA(cudaStreamWaitEvent(ds, evC[r], 0), "stream wait");
-    TB_CUDA(cudaMemcpyAsync(out_c + rb[r] * n, dC + rb[r] * n, (size_t)((rb[r + 1] - rb[r]) * n) * sizeof(double),
-                            cudaMemcpyDeviceToHost, ds),
-            "device to host copy");
+    started[r] = true;
+    if (--remaining[r] == 0) {
+      TB_CUDA(cudaEventRecord(evC[r], cs), "event record");
+      // D2H of block r as soon as it is final.
+      TB_CUDA(cudaStreamWaitEvent(ds, evC[r], 0), "stream wait");
+      TB_CUDA(cudaMemcpyAsync(out_c + rb[r] * n, dC + rb[r] * n, (size_t)((rb[r + 1] - rb[r]) * n) * sizeof(double),
+                              cudaMemcpyDeviceToHost, ds),
+              "device to host copy");
+    }
   }
   TB_CUDA(cudaEventRecord(e_end, ds), "event record");
   TB_CUDA(cudaEventSynchronize(e_end), "kernel execution");
-  TB_CUDA(cudaStreamSynchronize(cs), "kernel execution");
+  for (cudaStream_t cs : css) TB_CUDA(cudaStreamSynchronize(cs), "kernel execution");
   double ksum = 0.0;
   for (size_t i = 0; i < kt0.size(); ++i) {
     float ms = 0.f;
@@ -670,7 +714,7 @@ int tb_gpu_tiled_multiply_flat_ex(int32_t device, const double* a, const double*
   }
   float e_ms = 0.f;
   TB_CUDA(cudaEventElapsedTime(&e_ms, e_start, e_end), "event elapsed");
-  *out_seconds = ksum * 1e-3;  // kernel-only: sum of the GEMM launches
+  *out_seconds = ksum * 1e-3;  // kernel-only: sum of the GEMM launch durations
   if (out_e2e_seconds) *out_e2e_seconds = (double)e_ms * 1e-3;
   return TB_STATUS_OK;
 }
@@ -693,7 +737,7 @@ void tb_release(void) {
     st.ws_bytes = 0;
     if (st.cublas) cublasDestroy(st.cublas);
     st.cublas = nullptr;
-    for (cudaStream_t* sp : {&st.host_stream, &st.h2d_stream, &st.d2h_stream}) {
+    for (cudaStream_t* sp : {&st.host_stream, &st.host_stream2, &st.h2d_stream, &st.d2h_stream}) {
       if (*sp) cudaStreamDestroy(*sp);
       *sp = nullptr;
     }

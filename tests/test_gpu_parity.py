@@ -332,3 +332,32 @@ def test_n32768_sampled_exact_oracle(tb, oracle):
     assert rel <= NORMWISE
     del A, B, C, ref
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_shapes_property(tb, oracle, seed):
+    """Seeded random (m, k, n) in [1, 400]^3 x every variant: normwise and
+    elementwise bars vs the reference tiled oracle; the paper variant bitwise
+    vs the naive oracle."""
+    rng = np.random.Generator(np.random.PCG64(9000 + seed))
+    for _ in range(4):
+        m, k, n = (int(x) for x in rng.integers(1, 401, size=3))
+        a, b = oracle.generate(m, k, seed * 7 + m), oracle.generate(k, n, seed * 11 + n)
+        ref = oracle.tiled_parallel(a, b)
+        for v in FAST:
+            got = _gpu(tb, a, b, v)
+            assert oracle.normwise_rel(got, ref) <= NORMWISE, (m, k, n, v)
+            assert oracle.max_abs_rel_diff(got, ref) <= ELEMWISE, (m, k, n, v)
+        assert np.array_equal(_gpu(tb, a, b, "paper"), oracle.naive(a, b)), (m, k, n)
+
+
+def test_dimension_limits(tb):
+    lib = tb._lib.lib()
+    big = 2**31
+    assert lib.tb_validate_launch(big, 4, 4, 32, 0, 0) == tb.STATUS_OVER_LIMITS
+    assert lib.tb_validate_launch(4, big, 4, 32, 0, 0) == tb.STATUS_OVER_LIMITS
+    assert lib.tb_validate_launch(4, 4, 4, 33, 1, 0) == tb.STATUS_OVER_LIMITS  # 1089 threads (limits.test.ts)
+    assert lib.tb_validate_launch(4, 4, 4, 0, 0, 0) == tb.STATUS_BAD_DIMS
+    assert lib.tb_validate_launch(4, 4, 4, 32, 9, 0) == tb.STATUS_BAD_DIMS
+    assert lib.tb_validate_launch(4, 4, 4, 32, 0, 0) == tb.STATUS_OK
+    assert lib.tb_validate_launch(4, 4, 4, 32, 0, 999) == tb.STATUS_NO_DEVICE

@@ -356,6 +356,13 @@ __global__ void __launch_bounds__(DmmaCfg::THREADS, 1)
           for (int j = 0; j < C::NI; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i].y, bf[1][j]);
       }
       }
+      // Release the stage to the producer. The fragment loads above are
+      // generic-proxy reads that the next TMA (async proxy) into this stage
+      // must not overtake: without the proxy fence ptxas issues the arrive
+      // while the last LDS are still outstanding, and a TMA landing before
+      // they are serviced corrupts those fragments (observed on B200 when the
+      // accumulate epilogue's global loads back up the LSU queue).
+      fence_proxy_async();
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(&empty[s]));
       if (++s == STAGES) {
@@ -408,6 +415,54 @@ __global__ void __launch_bounds__(DmmaCfg::THREADS, 1)
     int tm, tn;
     tile_coords(tile, p.tiles_m, p.tiles_n, tm, tn);
     const int m0 = tm * C::BM, n0 = tn * C::BN;
+    if (p.accumulate && p.vec_store && m0 + C::BM <= p.m && n0 + C::BN <= p.n) {
+      // C += A·B on an interior tile: the old C values are fetched in two
+      // batches of 16 independent 16-byte loads (no branches, no stores in
+      // between), so the epilogue pays two memory round trips, not one per
+      // element.
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        double2 old[C::MI / 2][C::NI];
+#pragma unroll
+        for (int ii = 0; ii < C::MI / 2; ++ii) {
+          const double* crow = p.C + (int64_t)(m0 + row_base + (h * C::MI / 2 + ii) * row_step) * p.ldc;
+#pragma unroll
+          for (int j = 0; j < C::NI; ++j)
+            old[ii][j] = __ldcg(reinterpret_cast<const double2*>(crow + n0 + col_base + j * col_step));
+        }
+#pragma unroll
+        for (int ii = 0; ii < C::MI / 2; ++ii)
+#pragma unroll
+          for (int j = 0; j < C::NI; ++j) {
+            acc[h * C::MI / 2 + ii][j][0] += old[ii][j].x;
+            acc[h * C::MI / 2 + ii][j][1] += old[ii][j].y;
+          }
+      }
+    } else if (p.accumulate) {
+      // Edge tiles / unaligned rows: element-wise, bounds-checked.
+#pragma unroll
+      for (int i = 0; i < C::MI; ++i) {
+        const int r = m0 + row_base + i * row_step;
+        if (r >= p.m) continue;
+        const double* crow = p.C + (int64_t)r * p.ldc;
+#pragma unroll
+        for (int j = 0; j < C::NI; ++j) {
+          const int c = n0 + col_base + j * col_step;
+          if (c + 1 < p.n) {
+            if (p.vec_store) {
+              const double2 o = __ldcg(reinterpret_cast<const double2*>(crow + c));
+              acc[i][j][0] += o.x;
+              acc[i][j][1] += o.y;
+            } else {
+              acc[i][j][0] += __ldcg(crow + c);
+              acc[i][j][1] += __ldcg(crow + c + 1);
+            }
+          } else if (c < p.n) {
+            acc[i][j][0] += __ldcg(crow + c);
+          }
+        }
+      }
+    }
 #pragma unroll
     for (int i = 0; i < C::MI; ++i) {
       const int r = m0 + row_base + i * row_step;
@@ -416,12 +471,8 @@ __global__ void __launch_bounds__(DmmaCfg::THREADS, 1)
 #pragma unroll
       for (int j = 0; j < C::NI; ++j) {
         const int c = n0 + col_base + j * col_step;
-        double v0 = acc[i][j][0], v1 = acc[i][j][1];
+        const double v0 = acc[i][j][0], v1 = acc[i][j][1];
         if (c + 1 < p.n) {
-          if (p.accumulate) {
-            v0 += crow[c];
-            v1 += crow[c + 1];
-          }
           if (p.vec_store) {
             *reinterpret_cast<double2*>(crow + c) = make_double2(v0, v1);
           } else {
@@ -429,7 +480,7 @@ __global__ void __launch_bounds__(DmmaCfg::THREADS, 1)
             crow[c + 1] = v1;
           }
         } else if (c < p.n) {
-          crow[c] = p.accumulate ? v0 + crow[c] : v0;
+          crow[c] = v0;
         }
       }
     }

@@ -115,6 +115,7 @@ struct DeviceState {
     size_t counter_elems = 0;
   };
   std::map<cudaStream_t, SplitWs> split_ws;
+  std::vector<cudaEvent_t> ev_pool[2];  // host-buffer entry: [timing, no-timing] events
 };
 
 DeviceState g_dev[kMaxDevices];
@@ -317,6 +318,14 @@ int split_workspace(int dev, cudaStream_t stream, size_t partial_elems, size_t c
   DeviceState& st = g_dev[dev];
   std::lock_guard<std::mutex> lk(st.mu);
   DeviceState::SplitWs& w = st.split_ws[stream];
+  // Size for the schedule's bound on first use (plan_schedule: at most
+  // 2P - 1 stream-K tiles of at most 2 segments when T > P, at most P + T
+  // slots when T <= P), so a stream never regrows while its earlier launches
+  // may still be queued.
+  partial_elems = std::max(partial_elems, (size_t)4 * st.sms * tb::DmmaCfg::TILE_ELEMS);
+  counter_elems = std::max(counter_elems, (size_t)2 * st.sms);
+  if ((w.partial_elems < partial_elems && w.partials) || (w.counter_elems < counter_elems && w.counters))
+    TB_CUDA(cudaStreamSynchronize(stream), "stream-K workspace regrow");  // earlier launches may use it
   if (w.partial_elems < partial_elems) {
     if (w.partials) cudaFree(w.partials);
     w.partials = nullptr;
@@ -329,8 +338,10 @@ int split_workspace(int dev, cudaStream_t stream, size_t partial_elems, size_t c
     w.counters = nullptr;
     w.counter_elems = 0;
     TB_CUDA(cudaMalloc(&w.counters, counter_elems * sizeof(int)), "stream-K counter allocation");
-    // Counters start at zero once; each launch's last segment resets its tile's counter.
-    TB_CUDA(cudaMemset(w.counters, 0, counter_elems * sizeof(int)), "stream-K counter init");
+    // Counters start at zero once; each launch's last segment resets its tile's
+    // counter. Zeroed on the launching stream: a legacy-stream memset is not
+    // ordered before kernels on non-blocking streams.
+    TB_CUDA(cudaMemsetAsync(w.counters, 0, counter_elems * sizeof(int), stream), "stream-K counter init");
     w.counter_elems = counter_elems;
   }
   *partials = w.partials;
@@ -562,146 +573,192 @@ int tb_gpu_tiled_multiply_flat_ex(int32_t device, const double* a, const double*
   double* dB = dA + up(na);
   double* dC = dB + up(nb);
   const cudaStream_t hs = st.h2d_stream, ds = st.d2h_stream;
-  // Row blocks alternate between two compute streams so one launch's tail
-  // overlaps the next launch's head (blocks are independent).
   const cudaStream_t css[2] = {st.host_stream, st.host_stream2};
-  auto cs_of = [&](int r) { return css[r & 1]; };
 
-  // Copy/compute/copy pipeline over three streams (H2D, compute, D2H):
-  //  - R row blocks of A/C; P K-panels of B (contiguous row slices of B);
-  //  - the first Q row blocks are computed panel by panel as B's panels land
-  //    (C_r (+)= A_r[:, panel] · B[panel, :]), hiding B's transfer;
-  //  - later blocks run full-K while the next A block streams in and the
-  //    previous C block streams out.
-  // Small problems degenerate to one block / one panel (copy, GEMM, copy).
+  // Copy/compute/copy pipeline over four streams (H2D, two compute, D2H).
+  //  Phase 1 (rank-k panels): the first Mq rows of C are computed as
+  //    C[0:Mq] (+)= A[0:Mq, panel p] · B[panel p, :]
+  //  while the panels stream in (A's panel slice by a 2D copy, B's panel as
+  //  contiguous rows). The first panel is small, so the GEMM starts early;
+  //  Mq is sized so a panel's GEMM (2·Mq·kp·n flops) outlasts its transfer
+  //  (8·kp·(Mq+n) bytes) and compute does not wait on PCIe afterwards.
+  //  Phase 2 (row blocks): the remaining rows of A arrive as contiguous
+  //  blocks and run full-K GEMMs; every finished part of C is copied back at
+  //  once, and the last blocks shrink so the final D2H is short.
+  // Small problems degenerate to copy, GEMM, copy.
+  int64_t Mq = m;
+  std::vector<int64_t> pk{0, k};  // phase-1 K-panel bounds
+  std::vector<int64_t> gb{0, m};  // phase-1 row groups (one per compute stream)
+  std::vector<int64_t> rb{m};     // phase-2 row-block bounds, rb[0] = Mq
   const double flops = 2.0 * (double)m * (double)n * (double)k;
-  int R = 1, P = 1;
   if (flops >= 1e11) {
-    R = (int)std::min<int64_t>(8, std::max<int64_t>(1, m / 512));
-    P = (int)std::min<int64_t>(8, std::max<int64_t>(1, k / 256));
-  }
-  int Q = std::max(1, (R + 3) / 4);
-  // TB_PIPE=R,P,Q overrides the pipeline shape (tuning experiments).
-  if (const char* e = std::getenv("TB_PIPE")) {
-    int r = 0, pp = 0, qq = 0;
-    if (std::sscanf(e, "%d,%d,%d", &r, &pp, &qq) == 3 && r >= 1 && pp >= 1 && qq >= 1) {
-      R = (int)std::min<int64_t>(r, m);
-      P = (int)std::min<int64_t>(pp, std::max<int64_t>(1, k / 2));
-      Q = std::min(qq, R);
+    constexpr double kH2D = 55e9, kRate = 36e12;  // B/s (PCIe gen5 x16, measured), flop/s (FP64 DMMA)
+    const double den = (double)n * kH2D - 4.0 * kRate;
+    int64_t mq = den > 0 ? (int64_t)(1.2 * 4.0 * kRate * (double)n / den) : m;
+    int64_t kp0 = 256, kp_max = 2048, blk = 1024, groups = 2;
+    // TB_PIPE=mq,kp0,kp_max,blk[,groups] overrides the shape (tuning experiments).
+    if (const char* e = std::getenv("TB_PIPE")) {
+      long long a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 2;
+      if (std::sscanf(e, "%lld,%lld,%lld,%lld,%lld", &a0, &a1, &a2, &a3, &a4) >= 4 && a0 >= 1 && a1 >= 2 &&
+          a2 >= 2 && a3 >= 1 && a4 >= 1) {
+        mq = a0;
+        kp0 = a1;
+        kp_max = a2;
+        blk = a3;
+        groups = a4;
+      }
     }
+    mq = (mq + 127) / 128 * 128;
+    Mq = mq >= m - blk / 2 ? m : mq;
+    // Panel sizes: after a small first panel, each panel is as large as can
+    // land (transfer model) before the GEMMs queued so far drain (compute
+    // model), so the panels grow geometrically by the compute/transfer ratio
+    // without opening a compute gap; capped at kp_max.
+    const double tr_per_k = 8.0 * (double)(Mq + n) / kH2D, c_per_k = 2.0 * (double)Mq * (double)n / kRate;
+    pk.assign(1, 0);
+    double arrive = 0.0, finish = 0.0;
+    for (int64_t at = 0, step = kp0; at < k;) {
+      int64_t nx = at + step >= k - step / 2 ? k : ((at + step) & ~int64_t(1));  // even k0: TMA alignment
+      arrive += tr_per_k * (double)(nx - at);
+      finish = std::max(finish, arrive) + c_per_k * (double)(nx - at);
+      pk.push_back(nx);
+      at = nx;
+      step = std::min<int64_t>(kp_max, std::max<int64_t>(kp0, (int64_t)((finish - arrive) / tr_per_k)));
+    }
+    gb = (groups >= 2 && Mq >= 2048) ? std::vector<int64_t>{0, (Mq / 2 + 127) / 128 * 128, Mq}
+                                     : std::vector<int64_t>{0, Mq};
+    int64_t r = m - Mq;
+    std::vector<int64_t> tail;
+    for (int64_t t : {blk / 4, blk / 2})
+      if (t > 0 && r >= 2 * t) {
+        tail.push_back(t);
+        r -= t;
+      }
+    rb.assign(1, Mq);
+    const int64_t nb = (r + blk - 1) / blk;
+    for (int64_t i = 1; i <= nb; ++i) rb.push_back(Mq + r * i / nb);
+    for (auto it = tail.rbegin(); it != tail.rend(); ++it) rb.push_back(rb.back() + *it);
   }
-  std::vector<int64_t> rb(R + 1), pb(P + 1);
-  for (int r = 0; r <= R; ++r) rb[r] = m * r / R;
-  for (int p = 0; p <= P; ++p) pb[p] = (k * p / P) & ~int64_t(1);  // even k0 keeps TMA 16-byte alignment
-  pb[P] = k;
+  const int P = (int)pk.size() - 1, G = (int)gb.size() - 1, R = (int)rb.size() - 1;
 
-  std::vector<cudaEvent_t> evs;
+  // Events come from a per-device pool reused across calls (every call
+  // drains its streams before returning), so the host does not create and
+  // destroy ~100 events per call.
+  size_t used[2] = {0, 0};
+  bool ev_fail = false;
   auto mk = [&](unsigned flags) -> cudaEvent_t {
-    cudaEvent_t e = nullptr;
-    if (cudaEventCreateWithFlags(&e, flags) != cudaSuccess) return nullptr;
-    evs.push_back(e);
+    const int kind = flags == cudaEventDisableTiming ? 1 : 0;
+    std::vector<cudaEvent_t>& pool = st.ev_pool[kind];
+    if (used[kind] == pool.size()) {
+      cudaEvent_t e = nullptr;
+      if (cudaEventCreateWithFlags(&e, flags) != cudaSuccess) {
+        ev_fail = true;
+        return nullptr;
+      }
+      pool.push_back(e);
+    }
+    return pool[used[kind]++];
+  };
+  cudaEvent_t e_start = mk(cudaEventDefault), e_end = mk(cudaEventDefault);
+  std::vector<cudaEvent_t> evP(P), evA(R), kt0, kt1;
+  for (auto& e : evP) e = mk(cudaEventDisableTiming);
+  for (auto& e : evA) e = mk(cudaEventDisableTiming);
+  if (ev_fail) return cuda_fail(cudaGetLastError(), "event create");
+
+  // TB_PIPE_TRACE=1: print every copy / GEMM's device interval (ms from the
+  // pipeline start) to stderr — tooling for tools/pipe_trace.py.
+  static const bool trace = std::getenv("TB_PIPE_TRACE") != nullptr;
+  struct TraceRec {
+    const char* what;
+    int idx;
+    cudaEvent_t t0, t1;
+    double bytes;
+  };
+  std::vector<TraceRec> tr;
+  auto trace_begin = [&](cudaStream_t sm) -> cudaEvent_t {
+    if (!trace) return nullptr;
+    cudaEvent_t e = mk(cudaEventDefault);
+    if (e) cudaEventRecord(e, sm);
     return e;
   };
-  struct Cleanup {
-    std::vector<cudaEvent_t>& v;
-    ~Cleanup() {
-      for (auto e : v) cudaEventDestroy(e);
-    }
-  } cleanup{evs};
-  cudaEvent_t e_start = mk(cudaEventDefault), e_end = mk(cudaEventDefault);
-  std::vector<cudaEvent_t> evA(R), evB(P), evC(R), kt0, kt1;
-  for (auto& e : evA) e = mk(cudaEventDisableTiming);
-  for (auto& e : evB) e = mk(cudaEventDisableTiming);
-  for (auto& e : evC) e = mk(cudaEventDisableTiming);
-  for (auto e : evs)
-    if (!e) return cuda_fail(cudaGetLastError(), "event create");
-
-  auto h2d = [&](double* dst, const double* src, size_t elems, cudaEvent_t done) -> int {
-    TB_CUDA(cudaMemcpyAsync(dst, src, elems * sizeof(double), cudaMemcpyHostToDevice, hs), "host to device copy");
-    TB_CUDA(cudaEventRecord(done, hs), "event record");
+  auto trace_end = [&](const char* what, int idx, cudaEvent_t t0, cudaStream_t sm, double bytes) {
+    if (!trace || !t0) return;
+    cudaEvent_t e = mk(cudaEventDefault);
+    if (!e) return;
+    cudaEventRecord(e, sm);
+    tr.push_back({what, idx, t0, e, bytes});
+  };
+  // Rows [r0, r1) x columns [c0, c1) of a row-major host matrix with `cols`
+  // columns into the same place of its device copy (2D when c0..c1 is a slice).
+  auto h2d = [&](double* dst, const double* src, int64_t cols, int64_t r0, int64_t r1, int64_t c0, int64_t c1,
+                 const char* what, int idx) -> int {
+    cudaEvent_t t0 = trace_begin(hs);
+    const size_t pitch = (size_t)cols * sizeof(double);
+    if (c0 == 0 && c1 == cols)
+      TB_CUDA(cudaMemcpyAsync(dst + r0 * cols, src + r0 * cols, (size_t)(r1 - r0) * pitch, cudaMemcpyHostToDevice,
+                              hs),
+              "host to device copy");
+    else
+      TB_CUDA(cudaMemcpy2DAsync(dst + r0 * cols + c0, pitch, src + r0 * cols + c0, pitch,
+                                (size_t)(c1 - c0) * sizeof(double), (size_t)(r1 - r0), cudaMemcpyHostToDevice, hs),
+              "host to device copy");
+    trace_end(what, idx, t0, hs, (double)(r1 - r0) * (double)(c1 - c0) * sizeof(double));
     return TB_STATUS_OK;
   };
-  auto gemm = [&](int r, int64_t k0, int64_t k1, bool acc) -> int {
+  auto gemm = [&](cudaStream_t cs, int64_t r0, int64_t r1, int64_t k0, int64_t k1, bool acc) -> int {
     cudaEvent_t t0 = mk(cudaEventDefault), t1 = mk(cudaEventDefault);
     if (!t0 || !t1) return cuda_fail(cudaGetLastError(), "event create");
     kt0.push_back(t0);
     kt1.push_back(t1);
-    const int64_t r0 = rb[r], rows = rb[r + 1] - rb[r];
-    const cudaStream_t cs = cs_of(r);
     TB_CUDA(cudaEventRecord(t0, cs), "event record");
-    int rc = launch(device, dA + r0 * k + k0, k, dB + k0 * n, n, dC + r0 * n, n, rows, k1 - k0, n, acc ? 1 : 0,
+    int rc = launch(device, dA + r0 * k + k0, k, dB + k0 * n, n, dC + r0 * n, n, r1 - r0, k1 - k0, n, acc ? 1 : 0,
                     tile_edge, variant, cs);
     if (rc) return rc;
     TB_CUDA(cudaEventRecord(t1, cs), "event record");
+    return TB_STATUS_OK;
+  };
+  int nd2h = 0;
+  auto d2h = [&](cudaStream_t cs, int64_t r0, int64_t r1) -> int {
+    cudaEvent_t done = mk(cudaEventDisableTiming);
+    if (!done) return cuda_fail(cudaGetLastError(), "event create");
+    TB_CUDA(cudaEventRecord(done, cs), "event record");
+    TB_CUDA(cudaStreamWaitEvent(ds, done, 0), "stream wait");
+    cudaEvent_t t0 = trace_begin(ds);
+    TB_CUDA(cudaMemcpyAsync(out_c + r0 * n, dC + r0 * n, (size_t)((r1 - r0) * n) * sizeof(double),
+                            cudaMemcpyDeviceToHost, ds),
+            "device to host copy");
+    trace_end("d2h_C", nd2h++, t0, ds, (double)(r1 - r0) * n * sizeof(double));
     return TB_STATUS_OK;
   };
 
   TB_CUDA(cudaEventRecord(e_start, hs), "event record");
   for (cudaStream_t cs : css) TB_CUDA(cudaStreamWaitEvent(cs, e_start, 0), "stream wait");
   TB_CUDA(cudaStreamWaitEvent(ds, e_start, 0), "stream wait");
-  // H2D order: A0 B0 A1 B1 ... A(Q-1) B(Q-1), then the remaining B panels,
-  // then the remaining A blocks — the first compute cell (A0 x B0) is ready
-  // after two chunks and panel work grows as the transfers interleave.
-  struct Xfer {
-    bool is_a;
-    int idx;
-  };
-  std::vector<Xfer> order;
-  for (int i = 0; i < std::max(Q, P); ++i) {
-    if (i < Q) order.push_back({true, i});
-    if (i < P) order.push_back({false, i});
+  // H2D: phase-1 panels (A slice, then B rows), then the phase-2 row blocks.
+  for (int p = 0; p < P; ++p) {
+    if (Mq > 0 && (s = h2d(dA, a, k, 0, Mq, pk[p], pk[p + 1], "h2d_Ap", p))) return s;
+    if ((s = h2d(dB, b, n, pk[p], pk[p + 1], 0, n, "h2d_Bp", p))) return s;
+    TB_CUDA(cudaEventRecord(evP[p], hs), "event record");
   }
-  for (int r = Q; r < R; ++r) order.push_back({true, r});
-  std::vector<double> readyA(R), readyB(P);  // estimated arrival (bytes transferred so far)
-  double bytes = 0;
-  for (const Xfer& x : order) {
-    if (x.is_a) {
-      const int r = x.idx;
-      if ((s = h2d(dA + rb[r] * k, a + rb[r] * k, (size_t)((rb[r + 1] - rb[r]) * k), evA[r]))) return s;
-      bytes += (double)(rb[r + 1] - rb[r]) * k;
-      readyA[r] = bytes;
-    } else {
-      const int p = x.idx;
-      if ((s = h2d(dB + pb[p] * n, b + pb[p] * n, (size_t)((pb[p + 1] - pb[p]) * n), evB[p]))) return s;
-      bytes += (double)(pb[p + 1] - pb[p]) * n;
-      readyB[p] = bytes;
+  for (int r = 0; r < R; ++r) {
+    if ((s = h2d(dA, a, k, rb[r], rb[r + 1], 0, k, "h2d_A", r))) return s;
+    TB_CUDA(cudaEventRecord(evA[r], hs), "event record");
+  }
+  // Phase 1: panel p of every row group once it has landed; row group g
+  // stays on stream g, so its partial sums accumulate in panel order.
+  for (int p = 0; p < P; ++p)
+    for (int g = 0; g < G; ++g) {
+      TB_CUDA(cudaStreamWaitEvent(css[g], evP[p], 0), "stream wait");
+      if ((s = gemm(css[g], gb[g], gb[g + 1], pk[p], pk[p + 1], p > 0))) return s;
+      if (p == P - 1 && (s = d2h(css[g], gb[g], gb[g + 1]))) return s;
     }
-  }
-  // Compute cells in estimated data-ready order: (r, p) panel cells for the
-  // first Q row blocks, then full-K blocks. A row's cells share a stream, so
-  // its partial sums accumulate in enqueue order (first cell overwrites C).
-  struct Cell {
-    double ready;
-    int r, p;  // p < 0: full-K block
-  };
-  std::vector<Cell> cells;
-  for (int r = 0; r < Q; ++r)
-    for (int p = 0; p < P; ++p) cells.push_back({std::max(readyA[r], readyB[p]), r, p});
-  for (int r = Q; r < R; ++r) cells.push_back({std::max(readyA[r], readyB[P - 1]), r, -1});
-  std::stable_sort(cells.begin(), cells.end(), [](const Cell& x, const Cell& y) { return x.ready < y.ready; });
-  std::vector<int> remaining(R);
-  for (int r = 0; r < R; ++r) remaining[r] = r < Q ? P : 1;
-  std::vector<bool> started(R, false);
-  for (const Cell& cl : cells) {
-    const int r = cl.r;
-    const cudaStream_t cs = cs_of(r);
+  // Phase 2: full-K row blocks, alternating streams.
+  for (int r = 0; r < R; ++r) {
+    const cudaStream_t cs = css[r & 1];
+    TB_CUDA(cudaStreamWaitEvent(cs, evP[P - 1], 0), "stream wait");
     TB_CUDA(cudaStreamWaitEvent(cs, evA[r], 0), "stream wait");
-    if (cl.p >= 0) {
-      TB_CUDA(cudaStreamWaitEvent(cs, evB[cl.p], 0), "stream wait");
-      if ((s = gemm(r, pb[cl.p], pb[cl.p + 1], started[r]))) return s;
-    } else {
-      for (int p = 0; p < P; ++p) TB_CUDA(cudaStreamWaitEvent(cs, evB[p], 0), "stream wait");
-      if ((s = gemm(r, 0, k, false))) return s;
-    }
-    started[r] = true;
-    if (--remaining[r] == 0) {
-      TB_CUDA(cudaEventRecord(evC[r], cs), "event record");
-      // D2H of block r as soon as it is final.
-      TB_CUDA(cudaStreamWaitEvent(ds, evC[r], 0), "stream wait");
-      TB_CUDA(cudaMemcpyAsync(out_c + rb[r] * n, dC + rb[r] * n, (size_t)((rb[r + 1] - rb[r]) * n) * sizeof(double),
-                              cudaMemcpyDeviceToHost, ds),
-              "device to host copy");
-    }
+    if ((s = gemm(cs, rb[r], rb[r + 1], 0, k, false))) return s;
+    if ((s = d2h(cs, rb[r], rb[r + 1]))) return s;
   }
   TB_CUDA(cudaEventRecord(e_end, ds), "event record");
   TB_CUDA(cudaEventSynchronize(e_end), "kernel execution");
@@ -714,6 +771,15 @@ int tb_gpu_tiled_multiply_flat_ex(int32_t device, const double* a, const double*
   }
   float e_ms = 0.f;
   TB_CUDA(cudaEventElapsedTime(&e_ms, e_start, e_end), "event elapsed");
+  if (trace) {
+    for (size_t i = 0; i < kt0.size(); ++i) tr.push_back({"gemm", (int)i, kt0[i], kt1[i], 0.0});
+    for (const TraceRec& t : tr) {
+      float a0 = 0.f, a1 = 0.f;
+      cudaEventElapsedTime(&a0, e_start, t.t0);
+      cudaEventElapsedTime(&a1, e_start, t.t1);
+      std::fprintf(stderr, "TBTRACE %s %d %.4f %.4f %.0f\n", t.what, t.idx, a0, a1, t.bytes);
+    }
+  }
   *out_seconds = ksum * 1e-3;  // kernel-only: sum of the GEMM launch durations
   if (out_e2e_seconds) *out_e2e_seconds = (double)e_ms * 1e-3;
   return TB_STATUS_OK;
@@ -740,6 +806,10 @@ void tb_release(void) {
     for (cudaStream_t* sp : {&st.host_stream, &st.host_stream2, &st.h2d_stream, &st.d2h_stream}) {
       if (*sp) cudaStreamDestroy(*sp);
       *sp = nullptr;
+    }
+    for (auto& pool : st.ev_pool) {
+      for (cudaEvent_t e : pool) cudaEventDestroy(e);
+      pool.clear();
     }
     for (auto& kv : st.split_ws) {
       if (kv.second.partials) cudaFree(kv.second.partials);

@@ -267,10 +267,12 @@ def test_sharded_gemm_single_rank_nccl_panels(tb, oracle):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("m,k,n", [(4000, 4000, 4000), (3001, 2999, 2500)])
+@pytest.mark.parametrize("m,k,n", [(4000, 4000, 4000), (3001, 2999, 2500), (7000, 4999, 6000)])
 def test_flat_pipelined_host_path(tb, golden, oracle, m, k, n):
-    """Large host-buffer calls run the 3-stream copy/compute pipeline (row
-    blocks x K-panels); results must match the single-launch device path."""
+    """Large host-buffer calls run the copy/compute pipeline (phase 1: K-panels
+    of the first Mq rows with 2D copies of A's panel slices; phase 2: full-K
+    row blocks); results must match the single-launch device path. 7000 x
+    4999 x 6000 has an odd k (cp.async loader on panel views) and both phases."""
     import torch
 
     meta, g = golden
@@ -291,6 +293,50 @@ def test_flat_pipelined_host_path(tb, golden, oracle, m, k, n):
     c2 = np.zeros(m * n)
     assert tb.gpu_tiled_multiply_flat(0, a, b, m, k, n, 32, c2, out_s) == tb.STATUS_OK
     assert oracle.normwise_rel(c2.reshape(m, n), c_h.numpy()) <= NORMWISE
+
+
+@pytest.mark.parametrize("variant", ["dmma_tma", "dmma_cpasync", "dfma"])
+def test_accumulate_epilogue_many_tiles_per_cta(tb, variant):
+    """C += A·B with several tiles per persistent CTA (4096^2 outputs = 1024
+    tiles on 148 SMs), repeated: must equal the fp64 reference and be bitwise
+    reproducible. Regression test for a stage-release race (fragment loads
+    overtaken by the next TMA into the stage while the accumulate epilogue's
+    global loads back up the LSU queue) fixed with a proxy fence before the
+    empty-barrier arrive."""
+    import torch
+
+    g = torch.Generator(device="cuda").manual_seed(5)
+    m, k, n = 4096, 512, 4096
+    a = torch.rand((m, 2 * k), dtype=torch.float64, device="cuda", generator=g) + 2
+    b = torch.rand((2 * k, n), dtype=torch.float64, device="cuda", generator=g) + 2
+    ref = a @ b
+    first = a[:, :k] @ b[:k]
+    outs = []
+    for _ in range(3):
+        c = first.clone()
+        tb.dgemm_launch(a[:, k:], b[k:], c, accumulate=True, variant=variant)
+        torch.cuda.synchronize()
+        assert (torch.linalg.norm(c - ref) / torch.linalg.norm(ref)).item() <= NORMWISE
+        outs.append(c)
+    assert all(torch.equal(outs[0], o) for o in outs[1:])
+
+
+@pytest.mark.parametrize("shape", ["1024,128,640,384", "256,2,4000,4000", "100000,512,512,1"])
+def test_flat_pipeline_shapes(tb, oracle, monkeypatch, shape):
+    """Forced pipeline shapes (TB_PIPE=mq,kp0,kp,blk): many small panels and
+    blocks, a 2-wide first panel, all rows panelised — all equal the
+    single-launch result to the normwise bound."""
+    import torch
+
+    m, k, n = 4000, 3998, 4000
+    a, b = oracle.generate(m, k, 3), oracle.generate(k, n, 4)
+    monkeypatch.setenv("TB_PIPE", shape)
+    c = np.zeros(m * n)
+    out_s = np.zeros(1)
+    assert tb.gpu_tiled_multiply_flat(0, a, b, m, k, n, 32, c, out_s) == tb.STATUS_OK
+    ref, _ = tb.cublas_dgemm(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda())
+    got = torch.from_numpy(c.reshape(m, n)).cuda()
+    assert (torch.linalg.norm(got - ref) / torch.linalg.norm(ref)).item() <= NORMWISE
 
 
 def test_cli_run_writes_reference_csv(tb, tmp_path):

@@ -16,6 +16,10 @@ from .errors import InvalidConfigError, ShapeError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libtbgpu.so")
+# Tooling only (tools/kernel_timeline.py, A/B experiments): load another build
+# of the same sources, libtbgpu_<variant>.so, instead.
+if os.environ.get("TB_LIB_VARIANT"):
+    LIB_PATH = os.path.join(HERE, f"libtbgpu_{os.environ['TB_LIB_VARIANT']}.so")
 
 STATUS_OK = 0
 STATUS_BAD_DIMS = 1

@@ -46,22 +46,25 @@ def stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not stale():
+def build(force: bool = False, verbose: bool = False, timeline: bool = False) -> str:
+    """Build libtbgpu.so; ``timeline=True`` builds the instrumented tooling
+    variant libtbgpu_timeline.so (-DTB_TIMELINE: per-CTA %globaltimer stamps)."""
+    lib = LIB.replace("libtbgpu.so", "libtbgpu_timeline.so") if timeline else LIB
+    if not force and not timeline and not stale():
         return LIB
-    cmd = [nvcc(), *nvcc_flags(), *[os.path.join(CSRC, s) for s in SOURCES],
-           "-o", LIB + ".tmp", "-lcublas", "-Xlinker", "-rpath,/usr/local/cuda/lib64"]
+    cmd = [nvcc(), *nvcc_flags(), *(["-DTB_TIMELINE"] if timeline else []), *[os.path.join(CSRC, s) for s in SOURCES],
+           "-o", lib + ".tmp", "-lcublas", "-Xlinker", "-rpath,/usr/local/cuda/lib64"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     log = res.stdout + res.stderr
-    with open(os.path.join(HERE, "build.log"), "w") as f:
+    with open(os.path.join(HERE, "build_timeline.log" if timeline else "build.log"), "w") as f:
         f.write(" ".join(cmd) + "\n" + log)
     if res.returncode != 0:
         raise RuntimeError(f"nvcc failed:\n{log}")
-    os.replace(LIB + ".tmp", LIB)
+    os.replace(lib + ".tmp", lib)
     if verbose:
         print(log)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    print(build(force="--force" in sys.argv, verbose=True, timeline="--timeline" in sys.argv))

@@ -87,7 +87,21 @@ struct GemmParams {
   int max_seg;     // workspace slots per stream-K tile
   double* partials;  // [sk_tiles][max_seg][TILE_ELEMS] in fragment order
   int* counters;     // [sk_tiles], zero between launches (self-resetting)
+#ifdef TB_TIMELINE
+  unsigned long long* timeline;  // tooling build only: [grid][8] per-CTA %globaltimer stamps
+#endif
 };
+
+#ifdef TB_TIMELINE
+__device__ __forceinline__ unsigned long long tl_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define TB_TL(stmt) stmt
+#else
+#define TB_TL(stmt)
+#endif
 
 // Grouped raster over the (tile_m, tile_n) grid so concurrently resident CTAs
 // share A row-panels and B column-panels in L2.
@@ -147,6 +161,8 @@ __global__ void __launch_bounds__(DmmaCfg::THREADS, 1)
   int* flag = reinterpret_cast<int*>(empty + STAGES);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  TB_TL(unsigned long long* tl = p.timeline ? p.timeline + 8 * blockIdx.x : nullptr;)
+  TB_TL(if (tl && threadIdx.x == 0) tl[0] = tl_now();)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -294,8 +310,10 @@ __global__ void __launch_bounds__(DmmaCfg::THREADS, 1)
 #pragma unroll
       for (int j = 0; j < C::NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
+    TB_TL(unsigned long long tl_u = 0;)
     for (int kt = kb; kt < ke; ++kt) {
       mbar_wait(smem_u32(&full[s]), ph);
+      TB_TL(if (tl && ct == 0 && kt == kb) { tl_u = tl_now(); if (tl[1] == 0) tl[1] = tl_u; })
       if constexpr (MT == Math::DFMA) {
 #pragma unroll
         for (int u = 0; u < SUB; ++u) {
@@ -371,6 +389,8 @@ __global__ void __launch_bounds__(DmmaCfg::THREADS, 1)
       }
     }
 
+    TB_TL(const unsigned long long tl_m = tl && ct == 0 ? tl_now() : 0;)
+    TB_TL(if (tl && ct == 0) { tl[2] = tl_m; tl[4] += 1; tl[7] += tl_m - tl_u; })
     // ------------------------------------------------- stream-K segment fixup
     if (kb != 0 || ke != p.num_k) {
       const int st = tile - p.dp_tiles;
@@ -390,7 +410,10 @@ __global__ void __launch_bounds__(DmmaCfg::THREADS, 1)
       consumer_bar();
       const bool last = (*flag == nseg - 1);
       consumer_bar();  // flag is reused by the next unit
-      if (!last) continue;
+      if (!last) {
+        TB_TL(if (tl && ct == 0) { const unsigned long long t = tl_now(); tl[5] += t - tl_m; tl[3] = t; })
+        continue;
+      }
       __threadfence();
       // Deterministic reduction: all segments (own one re-read from L2 too)
       // summed in index order 0..nseg-1, whichever CTA finishes last.
@@ -412,6 +435,8 @@ __global__ void __launch_bounds__(DmmaCfg::THREADS, 1)
     }
 
     // --------------------------------------------------------------- epilogue
+    TB_TL(const unsigned long long tl_e = tl && ct == 0 ? tl_now() : 0;)
+    TB_TL(if (tl && ct == 0) tl[5] += tl_e - tl_m;)
     int tm, tn;
     tile_coords(tile, p.tiles_m, p.tiles_n, tm, tn);
     const int m0 = tm * C::BM, n0 = tn * C::BN;
@@ -484,6 +509,7 @@ __global__ void __launch_bounds__(DmmaCfg::THREADS, 1)
         }
       }
     }
+    TB_TL(if (tl && ct == 0) { const unsigned long long t = tl_now(); tl[6] += t - tl_e; tl[3] = t; })
   }
 }
 

@@ -393,6 +393,15 @@ int launch(int dev, const double* A, int64_t lda, const double* B, int64_t ldb, 
     p.max_seg = sc.max_seg;
     p.partials = nullptr;
     p.counters = nullptr;
+#ifdef TB_TIMELINE
+    unsigned long long* tl_buf = nullptr;
+    p.timeline = nullptr;
+    if (std::getenv("TB_TIMELINE")) {
+      TB_CUDA(cudaMalloc(&tl_buf, (size_t)sc.grid * 8 * sizeof(unsigned long long)), "timeline alloc");
+      TB_CUDA(cudaMemsetAsync(tl_buf, 0, (size_t)sc.grid * 8 * sizeof(unsigned long long), stream), "timeline");
+      p.timeline = tl_buf;
+    }
+#endif
     if (sc.sk > 0 &&
         (s = split_workspace(dev, stream, (size_t)sc.sk * sc.max_seg * Cfg::TILE_ELEMS, (size_t)sc.sk, &p.partials,
                              &p.counters)))
@@ -410,6 +419,42 @@ int launch(int dev, const double* A, int64_t lda, const double* B, int64_t ldb, 
     TB_CUDA(cudaLaunchKernel(cfg_kernel(cfg, use_tma, dfma), dim3((unsigned)sc.grid), dim3(Cfg::THREADS), args,
                              (size_t)cfg_smem(cfg), stream),
             "kernel launch");
+#ifdef TB_TIMELINE
+    if (tl_buf) {
+      // Per-CTA stamps (ns): [0] entry [1] first stage landed [2] last main-loop end [3] last unit done
+      // [4] units [5] fixup ns [6] epilogue ns [7] main-loop ns.
+      std::vector<unsigned long long> h((size_t)sc.grid * 8);
+      TB_CUDA(cudaStreamSynchronize(stream), "timeline sync");
+      TB_CUDA(cudaMemcpy(h.data(), tl_buf, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost), "tl");
+      cudaFree(tl_buf);
+      unsigned long long t0 = ~0ull, tend = 0;
+      double first = 0, mainl = 0, fix = 0, epi = 0, units = 0, endmax = 0, endmin = 1e30, lastml = 0;
+      for (int c = 0; c < sc.grid; ++c) {
+        const unsigned long long* r = &h[(size_t)c * 8];
+        t0 = std::min(t0, r[0]);
+        tend = std::max(tend, r[3]);
+      }
+      for (int c = 0; c < sc.grid; ++c) {
+        const unsigned long long* r = &h[(size_t)c * 8];
+        first += (double)(r[1] - t0);
+        lastml += (double)(r[2] - t0);
+        mainl += (double)r[7];
+        fix += (double)r[5];
+        epi += (double)r[6];
+        units += (double)r[4];
+        endmax = std::max(endmax, (double)(r[3] - t0));
+        endmin = std::min(endmin, (double)(r[3] - t0));
+      }
+      const double g = sc.grid;
+      std::fprintf(stderr,
+                   "TBTIMELINE m=%lld n=%lld k=%lld grid=%d dp=%d sk=%d ipc=%d maxseg=%d span_us=%.2f "
+                   "first_stage_us=%.2f mainloop_us=%.2f last_mainloop_end_us=%.2f fixup_us=%.2f epilogue_us=%.2f "
+                   "units=%.2f end_min_us=%.2f end_max_us=%.2f\n",
+                   (long long)m, (long long)n, (long long)k, sc.grid, sc.dp, sc.sk, sc.ipc, sc.max_seg,
+                   (tend - t0) / 1e3, first / g / 1e3, mainl / g / 1e3, lastml / g / 1e3, fix / g / 1e3,
+                   epi / g / 1e3, units / g, endmin / 1e3, endmax / 1e3);
+    }
+#endif
   }
   TB_CUDA(cudaGetLastError(), "kernel launch");
   return TB_STATUS_OK;

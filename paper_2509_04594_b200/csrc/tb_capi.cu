@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <chrono>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -591,6 +592,7 @@ int tb_dgemm_launch(const double* A, int64_t lda, const double* B, int64_t ldb, 
 int tb_gpu_tiled_multiply_flat_ex(int32_t device, const double* a, const double* b, int64_t m, int64_t k, int64_t n,
                                   int32_t tile_edge, int32_t variant, double* out_c, int64_t out_c_len,
                                   double* out_seconds, double* out_e2e_seconds) {
+  const auto h_entry = std::chrono::steady_clock::now();
   int s = check_device(device);  // multiply.ts:65 — no device is a status, not a throw
   if (s) return s;
   if (!a || !b || !out_c || !out_seconds || m < 1 || k < 1 || n < 1 || out_c_len != m * n) {
@@ -640,7 +642,7 @@ int tb_gpu_tiled_multiply_flat_ex(int32_t device, const double* a, const double*
     constexpr double kH2D = 55e9, kRate = 36e12;  // B/s (PCIe gen5 x16, measured), flop/s (FP64 DMMA)
     const double den = (double)n * kH2D - 4.0 * kRate;
     int64_t mq = den > 0 ? (int64_t)(1.2 * 4.0 * kRate * (double)n / den) : m;
-    int64_t kp0 = 256, kp_max = 2048, blk = 1024, groups = 2;
+    int64_t kp0 = 256, kp_max = 2048, blk = 1536, groups = 2;
     // TB_PIPE=mq,kp0,kp_max,blk[,groups] overrides the shape (tuning experiments).
     if (const char* e = std::getenv("TB_PIPE")) {
       long long a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 2;
@@ -674,7 +676,7 @@ int tb_gpu_tiled_multiply_flat_ex(int32_t device, const double* a, const double*
                                      : std::vector<int64_t>{0, Mq};
     int64_t r = m - Mq;
     std::vector<int64_t> tail;
-    for (int64_t t : {blk / 4, blk / 2})
+    for (int64_t t : {std::min<int64_t>(256, blk / 4), blk / 2})  // shrinking tail: the last D2H is <= 20 MB
       if (t > 0 && r >= 2 * t) {
         tail.push_back(t);
         r -= t;
@@ -776,6 +778,7 @@ int tb_gpu_tiled_multiply_flat_ex(int32_t device, const double* a, const double*
     return TB_STATUS_OK;
   };
 
+  const auto h_start = std::chrono::steady_clock::now();
   TB_CUDA(cudaEventRecord(e_start, hs), "event record");
   for (cudaStream_t cs : css) TB_CUDA(cudaStreamWaitEvent(cs, e_start, 0), "stream wait");
   TB_CUDA(cudaStreamWaitEvent(ds, e_start, 0), "stream wait");
@@ -806,8 +809,20 @@ int tb_gpu_tiled_multiply_flat_ex(int32_t device, const double* a, const double*
     if ((s = d2h(cs, rb[r], rb[r + 1]))) return s;
   }
   TB_CUDA(cudaEventRecord(e_end, ds), "event record");
-  TB_CUDA(cudaEventSynchronize(e_end), "kernel execution");
+  const auto h_enq = std::chrono::steady_clock::now();
+  // The call is synchronous: spin on the last D2H's event rather than a
+  // blocking wait, whose wake-up latency would add to every call.
+  static const bool block_sync = std::getenv("TB_SYNC_BLOCK") != nullptr;
+  if (block_sync) {
+    TB_CUDA(cudaEventSynchronize(e_end), "kernel execution");
+  } else {
+    cudaError_t q;
+    while ((q = cudaEventQuery(e_end)) == cudaErrorNotReady) {
+    }
+    TB_CUDA(q, "kernel execution");
+  }
   for (cudaStream_t cs : css) TB_CUDA(cudaStreamSynchronize(cs), "kernel execution");
+  const auto h_sync = std::chrono::steady_clock::now();
   double ksum = 0.0;
   for (size_t i = 0; i < kt0.size(); ++i) {
     float ms = 0.f;
@@ -817,6 +832,12 @@ int tb_gpu_tiled_multiply_flat_ex(int32_t device, const double* a, const double*
   float e_ms = 0.f;
   TB_CUDA(cudaEventElapsedTime(&e_ms, e_start, e_end), "event elapsed");
   if (trace) {
+    auto us = [](std::chrono::steady_clock::time_point x, std::chrono::steady_clock::time_point y) {
+      return std::chrono::duration<double, std::micro>(y - x).count();
+    };
+    std::fprintf(stderr, "TBHOST entry_to_start_us %.1f enqueue_us %.1f wait_us %.1f post_us %.1f\n",
+                 us(h_entry, h_start), us(h_start, h_enq), us(h_enq, h_sync),
+                 us(h_sync, std::chrono::steady_clock::now()));
     for (size_t i = 0; i < kt0.size(); ++i) tr.push_back({"gemm", (int)i, kt0[i], kt1[i], 0.0});
     for (const TraceRec& t : tr) {
       float a0 = 0.f, a1 = 0.f;

@@ -91,13 +91,14 @@ def main():
         if sh != "default":
             env["TB_PIPE"] = sh
         out = subprocess.run([sys.executable, "-c", CODE, str(n)], env=env, capture_output=True, text=True)
-        lines = [ln for ln in out.stderr.splitlines() if ln.split() and ln.split()[0] in ("CALL", "TBTRACE", "E2E")]
+        lines = [ln for ln in out.stderr.splitlines() if ln.split() and ln.split()[0] in ("CALL", "TBTRACE", "E2E", "TBHOST")]
         e2e = [float(ln.split()[2]) for ln in lines if ln.startswith("E2E")]
         wall = [float(ln.split()[3]) for ln in lines if ln.startswith("E2E")]
         if not e2e:
             print(sh, out.stderr[-800:])
             continue
         recs, summ = analyse(lines, 2)
+        summ["host"] = [ln for ln in lines if ln.startswith("TBHOST")][-1:]
         print(json.dumps({"pipe": sh, "n": n, "e2e_ms": e2e, "wall_ms": wall, **summ}))
         for r in sorted(recs, key=lambda r: r[2]):
             gbs = r[4] / ((r[3] - r[2]) * 1e-3) / 1e9 if r[4] else 0.0

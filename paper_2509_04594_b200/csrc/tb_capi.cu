@@ -283,25 +283,53 @@ int check_device(int32_t device) {
 }
 
 // Persistent schedule (dgemm_dmma.cuh): data-parallel tiles round-robin over
-// P = #SM CTAs, then the last (T mod P) + P tiles as stream-K k-iterations
-// split evenly across the CTAs. TB_SCHED=dp disables the stream-K region.
+// the CTAs, then a stream-K region whose k-iterations are split evenly across
+// them. Three shapes, chosen on the host (the kernel is the same):
+//  - stream-K: the last (T mod P) + P tiles split over P = #SM CTAs;
+//  - data-parallel: no split when a single wave is >= 90 % full — splitting
+//    every tile costs partial-tile traffic and fixups that an idle 10 % does
+//    not (measured: with several waves the stream-K tail still wins);
+//  - split-K: T <= P/2 tiles each split into exactly s = P / T equal k-ranges
+//    on s*T CTAs (num_k padded up to a multiple of s with k-slabs past K,
+//    which the loaders zero-fill), so every CTA owns exactly one segment and
+//    every tile exactly s — the stream-K split of so few tiles would give
+//    3-4 segments per tile and two fixups to some CTAs.
+// TB_SCHED=dp|sk forces data-parallel / the plain stream-K shape (A/B experiments).
 struct Schedule {
-  int grid, dp, sk, ipc, max_seg;
+  int grid, dp, sk, ipc, max_seg, num_k;
 };
 
 Schedule plan_schedule(int64_t tiles, int num_k, int sms) {
-  static const bool dp_only = [] {
+  static const int forced = [] {
     const char* e = std::getenv("TB_SCHED");
-    return e && std::strcmp(e, "dp") == 0;
+    if (e && std::strcmp(e, "dp") == 0) return 1;
+    if (e && std::strcmp(e, "sk") == 0) return 2;  // always the stream-K shape (previous default)
+    return 0;
   }();
-  Schedule sc{sms, (int)tiles, 0, 1, 1};
+  Schedule sc{sms, (int)tiles, 0, 1, 1, num_k};
   const int64_t rem = tiles % sms;
-  if (dp_only || rem == 0) return sc;
+  if (forced == 1 || rem == 0) return sc;
+  // A single wave >= 90 % full runs data-parallel (N = 1500: 144 tiles, 28.6 -> 31.2 TFLOP/s); with
+  // more waves the stream-K tail stays ahead (N = 4000 / 6000 at 92 %: 34.12 / 35.84 vs 33.99 / 35.76).
+  if (forced == 0 && tiles < sms && 10 * tiles >= 9 * sms) return sc;
+  const int64_t min_seg = num_k < 8 ? num_k : 8;      // keep segments long enough to amortise the fixup
+  if (forced == 0 && 2 * tiles <= sms) {
+    int64_t split = std::min<int64_t>(sms / tiles, num_k / min_seg);
+    if (split >= 2) {
+      const int64_t ipc = (num_k + split - 1) / split;
+      sc.num_k = (int)(ipc * split);
+      sc.grid = (int)(split * tiles);
+      sc.dp = 0;
+      sc.sk = (int)tiles;
+      sc.ipc = (int)ipc;
+      sc.max_seg = (int)split;
+      return sc;
+    }
+  }
   sc.sk = (int)(tiles > sms ? rem + sms : tiles);
   sc.dp = (int)(tiles - sc.sk);
   const int64_t total = (int64_t)sc.sk * num_k;
   int64_t ipc = (total + sms - 1) / sms;
-  const int64_t min_seg = num_k < 8 ? num_k : 8;  // keep segments long enough to amortise the fixup
   if (ipc < min_seg) ipc = min_seg;
   sc.ipc = (int)ipc;
   int max_seg = 1;
@@ -388,6 +416,7 @@ int launch(int dev, const double* A, int64_t lda, const double* B, int64_t ldb, 
     const int64_t kstage = (int64_t)Cfg::BK * kCfgs[cfg].sub;
     p.num_k = (int)((k + kstage - 1) / kstage);
     const Schedule sc = plan_schedule(tiles, p.num_k, g_dev[dev].sms);
+    p.num_k = sc.num_k;  // split-K pads the k-slab count (extra slabs read as zeros)
     p.dp_tiles = sc.dp;
     p.sk_tiles = sc.sk;
     p.sk_ipc = sc.ipc;

@@ -295,6 +295,20 @@ def test_flat_pipelined_host_path(tb, golden, oracle, m, k, n):
     assert oracle.normwise_rel(c2.reshape(m, n), c_h.numpy()) <= NORMWISE
 
 
+@pytest.mark.parametrize("m,k,n", [(1000, 777, 1000), (500, 1000, 500), (640, 1010, 384), (1500, 1500, 1500),
+                                   (1100, 900, 1100)])
+@pytest.mark.parametrize("variant", FAST)
+def test_schedule_shapes(tb, oracle, m, k, n, variant):
+    """Each host-side schedule shape against the oracle: split-K with k-slabs
+    padded past K (1000x777x1000: 64 tiles, s = 2, 49 -> 50 slabs), split-K
+    without padding (500x1000x500, 640x1010x384), a >= 90 % single wave run
+    data-parallel (1500^3: 144 tiles) and plain stream-K (1100^3: 81 tiles)."""
+    a, b = oracle.generate(m, k, 11), oracle.generate(k, n, 12)
+    got, sec = tb.gpu_tiled_multiply_timed(a, b, variant=variant)
+    assert sec > 0
+    assert oracle.normwise_rel(got, oracle.tiled_parallel(a, b)) <= NORMWISE
+
+
 @pytest.mark.parametrize("variant", ["dmma_tma", "dmma_cpasync", "dfma"])
 def test_accumulate_epilogue_many_tiles_per_cta(tb, variant):
     """C += A·B with several tiles per persistent CTA (4096^2 outputs = 1024

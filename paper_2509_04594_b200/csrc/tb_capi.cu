@@ -116,6 +116,11 @@ struct DeviceState {
     size_t counter_elems = 0;
   };
   std::map<cudaStream_t, SplitWs> split_ws;
+  struct StageWs {  // even-pitch copies of misaligned operands (TMA staging), per stream
+    double* buf = nullptr;
+    size_t elems = 0;
+  };
+  std::map<cudaStream_t, StageWs> stage_ws;
   std::vector<cudaEvent_t> ev_pool[2];  // host-buffer entry: [timing, no-timing] events
 };
 
@@ -379,10 +384,88 @@ int split_workspace(int dev, cudaStream_t stream, size_t partial_elems, size_t c
 }
 
 // Enqueue one GEMM on `stream` (current device = dev). Assumes validated args.
+// AUTO on operands TMA cannot address (odd leading dimension or a base not
+// 16-byte aligned — the reference's odd-N cases) would run the cp.async
+// loader at ~92 % of the TMA path's speed. For large products the operands
+// are instead copied once, on the launching stream, into even-pitch
+// workspace buffers (HBM copy: ~1 % of the GEMM time at N = 9999) and the
+// TMA kernel runs on those. Small products keep the cp.async loader.
+constexpr double kStageMinFlops = 2e10;
+constexpr size_t kStageMaxBytes = size_t(16) << 30;
+
+// Row re-pitch for staging: dst (16-byte aligned, even pitch) <- src (any
+// 8-byte alignment/pitch). One block row-slab per blockIdx.y, coalesced 8-byte
+// loads, 16-byte stores where the destination allows.
+__global__ void __launch_bounds__(256) repitch_kernel(const double* __restrict__ src, int64_t lds,
+                                                      double* __restrict__ dst, int64_t ldd, int64_t rows,
+                                                      int64_t cols) {
+  for (int64_t r = blockIdx.y; r < rows; r += gridDim.y) {
+    const double* s = src + r * lds;
+    double2* d = reinterpret_cast<double2*>(dst + r * ldd);
+    for (int64_t c = 2 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x); c < cols;
+         c += 2 * (int64_t)gridDim.x * blockDim.x) {
+      const double x = s[c];
+      const double y = c + 1 < cols ? s[c + 1] : 0.0;
+      d[c >> 1] = make_double2(x, y);  // ldd even and >= cols + (cols & 1): the pad column takes 0
+    }
+  }
+}
+
+int repitch(const double* src, int64_t lds, double* dst, int64_t ldd, int64_t rows, int64_t cols,
+            cudaStream_t stream) {
+  const int64_t pairs = (cols + 1) / 2;
+  const unsigned gx = (unsigned)std::min<int64_t>((pairs + 255) / 256, 8);
+  const unsigned gy = (unsigned)std::min<int64_t>(rows, 65535);
+  repitch_kernel<<<dim3(gx, gy), 256, 0, stream>>>(src, lds, dst, ldd, rows, cols);
+  TB_CUDA(cudaGetLastError(), "staging copy launch");
+  return TB_STATUS_OK;
+}
+
+bool misaligned(const void* p, int64_t ld) { return (reinterpret_cast<uintptr_t>(p) & 15u) != 0 || (ld % 2) != 0; }
+
+int stage_workspace(int dev, cudaStream_t stream, size_t elems, double** buf) {
+  DeviceState& st = g_dev[dev];
+  std::lock_guard<std::mutex> lk(st.mu);
+  DeviceState::StageWs& w = st.stage_ws[stream];
+  if (w.elems < elems) {
+    if (w.buf) {
+      TB_CUDA(cudaStreamSynchronize(stream), "staging workspace regrow");  // earlier launches may use it
+      cudaFree(w.buf);
+    }
+    w.buf = nullptr;
+    w.elems = 0;
+    TB_CUDA(cudaMalloc(&w.buf, elems * sizeof(double)), "staging workspace allocation");
+    w.elems = elems;
+  }
+  *buf = w.buf;
+  return TB_STATUS_OK;
+}
+
 int launch(int dev, const double* A, int64_t lda, const double* B, int64_t ldb, double* Cm, int64_t ldc, int64_t m,
            int64_t k, int64_t n, int accumulate, int tile_edge, int variant, cudaStream_t stream) {
   int s = ensure_kernel_attrs(dev);
   if (s) return s;
+  if (variant == TB_VARIANT_AUTO && !tma_ok(A, lda, B, ldb) && 2.0 * (double)m * (double)n * (double)k >= kStageMinFlops) {
+    const bool sa = misaligned(A, lda), sb = misaligned(B, ldb);
+    const int64_t lda2 = (k + 1) & ~int64_t(1), ldb2 = (n + 1) & ~int64_t(1);
+    const size_t ea = sa ? (size_t)(m * lda2 + 32) : 0, eb = sb ? (size_t)(k * ldb2) : 0;
+    if ((ea + eb) * sizeof(double) <= kStageMaxBytes) {
+      double* buf = nullptr;
+      if ((s = stage_workspace(dev, stream, ea + eb + 32, &buf))) return s;
+      double* a2 = buf;
+      double* b2 = buf + ((ea + 31) & ~size_t(31));  // 256-byte aligned
+      if (sa) {
+        if ((s = repitch(A, lda, a2, lda2, m, k, stream))) return s;
+        A = a2;
+        lda = lda2;
+      }
+      if (sb) {
+        if ((s = repitch(B, ldb, b2, ldb2, k, n, stream))) return s;
+        B = b2;
+        ldb = ldb2;
+      }
+    }
+  }
   variant = resolve(A, lda, B, ldb, variant);
   if (variant == TB_VARIANT_PAPER) {
     const int K = tile_edge;
@@ -633,7 +716,10 @@ int tb_gpu_tiled_multiply_flat_ex(int32_t device, const double* a, const double*
   DeviceGuard guard(device);
   DeviceState& st = g_dev[device];
   std::lock_guard<std::mutex> lk(st.host_mu);  // one in-flight call per backend
-  const size_t na = (size_t)(m * k), nb = (size_t)(k * n), nc = (size_t)(m * n);
+  // Device copies use even pitches so odd k / n still get the TMA loader and
+  // 16-byte C stores / batched accumulate loads (the 2D copies re-pitch for free).
+  const int64_t lda_d = (k + 1) & ~int64_t(1), ldb_d = (n + 1) & ~int64_t(1), ldc_d = ldb_d;
+  const size_t na = (size_t)(m * lda_d), nb = (size_t)(k * ldb_d), nc = (size_t)(m * ldc_d);
   auto up = [](size_t x) { return (x + 31) & ~size_t(31); };  // 256-byte aligned sub-buffers
   const size_t need = (up(na) + up(nb) + up(nc)) * sizeof(double);
   for (cudaStream_t* sp : {&st.host_stream, &st.host_stream2, &st.h2d_stream, &st.d2h_stream})
@@ -765,17 +851,17 @@ int tb_gpu_tiled_multiply_flat_ex(int32_t device, const double* a, const double*
     tr.push_back({what, idx, t0, e, bytes});
   };
   // Rows [r0, r1) x columns [c0, c1) of a row-major host matrix with `cols`
-  // columns into the same place of its device copy (2D when c0..c1 is a slice).
-  auto h2d = [&](double* dst, const double* src, int64_t cols, int64_t r0, int64_t r1, int64_t c0, int64_t c1,
-                 const char* what, int idx) -> int {
+  // columns into the same place of its device copy of pitch `dld` (>= cols).
+  auto h2d = [&](double* dst, int64_t dld, const double* src, int64_t cols, int64_t r0, int64_t r1, int64_t c0,
+                 int64_t c1, const char* what, int idx) -> int {
     cudaEvent_t t0 = trace_begin(hs);
     const size_t pitch = (size_t)cols * sizeof(double);
-    if (c0 == 0 && c1 == cols)
+    if (c0 == 0 && c1 == cols && dld == cols)
       TB_CUDA(cudaMemcpyAsync(dst + r0 * cols, src + r0 * cols, (size_t)(r1 - r0) * pitch, cudaMemcpyHostToDevice,
                               hs),
               "host to device copy");
     else
-      TB_CUDA(cudaMemcpy2DAsync(dst + r0 * cols + c0, pitch, src + r0 * cols + c0, pitch,
+      TB_CUDA(cudaMemcpy2DAsync(dst + r0 * dld + c0, (size_t)dld * sizeof(double), src + r0 * cols + c0, pitch,
                                 (size_t)(c1 - c0) * sizeof(double), (size_t)(r1 - r0), cudaMemcpyHostToDevice, hs),
               "host to device copy");
     trace_end(what, idx, t0, hs, (double)(r1 - r0) * (double)(c1 - c0) * sizeof(double));
@@ -787,8 +873,8 @@ int tb_gpu_tiled_multiply_flat_ex(int32_t device, const double* a, const double*
     kt0.push_back(t0);
     kt1.push_back(t1);
     TB_CUDA(cudaEventRecord(t0, cs), "event record");
-    int rc = launch(device, dA + r0 * k + k0, k, dB + k0 * n, n, dC + r0 * n, n, r1 - r0, k1 - k0, n, acc ? 1 : 0,
-                    tile_edge, variant, cs);
+    int rc = launch(device, dA + r0 * lda_d + k0, lda_d, dB + k0 * ldb_d, ldb_d, dC + r0 * ldc_d, ldc_d, r1 - r0,
+                    k1 - k0, n, acc ? 1 : 0, tile_edge, variant, cs);
     if (rc) return rc;
     TB_CUDA(cudaEventRecord(t1, cs), "event record");
     return TB_STATUS_OK;
@@ -800,9 +886,15 @@ int tb_gpu_tiled_multiply_flat_ex(int32_t device, const double* a, const double*
     TB_CUDA(cudaEventRecord(done, cs), "event record");
     TB_CUDA(cudaStreamWaitEvent(ds, done, 0), "stream wait");
     cudaEvent_t t0 = trace_begin(ds);
-    TB_CUDA(cudaMemcpyAsync(out_c + r0 * n, dC + r0 * n, (size_t)((r1 - r0) * n) * sizeof(double),
-                            cudaMemcpyDeviceToHost, ds),
-            "device to host copy");
+    if (ldc_d == n)
+      TB_CUDA(cudaMemcpyAsync(out_c + r0 * n, dC + r0 * n, (size_t)((r1 - r0) * n) * sizeof(double),
+                              cudaMemcpyDeviceToHost, ds),
+              "device to host copy");
+    else
+      TB_CUDA(cudaMemcpy2DAsync(out_c + r0 * n, (size_t)n * sizeof(double), dC + r0 * ldc_d,
+                                (size_t)ldc_d * sizeof(double), (size_t)n * sizeof(double), (size_t)(r1 - r0),
+                                cudaMemcpyDeviceToHost, ds),
+              "device to host copy");
     trace_end("d2h_C", nd2h++, t0, ds, (double)(r1 - r0) * n * sizeof(double));
     return TB_STATUS_OK;
   };
@@ -813,12 +905,12 @@ int tb_gpu_tiled_multiply_flat_ex(int32_t device, const double* a, const double*
   TB_CUDA(cudaStreamWaitEvent(ds, e_start, 0), "stream wait");
   // H2D: phase-1 panels (A slice, then B rows), then the phase-2 row blocks.
   for (int p = 0; p < P; ++p) {
-    if (Mq > 0 && (s = h2d(dA, a, k, 0, Mq, pk[p], pk[p + 1], "h2d_Ap", p))) return s;
-    if ((s = h2d(dB, b, n, pk[p], pk[p + 1], 0, n, "h2d_Bp", p))) return s;
+    if (Mq > 0 && (s = h2d(dA, lda_d, a, k, 0, Mq, pk[p], pk[p + 1], "h2d_Ap", p))) return s;
+    if ((s = h2d(dB, ldb_d, b, n, pk[p], pk[p + 1], 0, n, "h2d_Bp", p))) return s;
     TB_CUDA(cudaEventRecord(evP[p], hs), "event record");
   }
   for (int r = 0; r < R; ++r) {
-    if ((s = h2d(dA, a, k, rb[r], rb[r + 1], 0, k, "h2d_A", r))) return s;
+    if ((s = h2d(dA, lda_d, a, k, rb[r], rb[r + 1], 0, k, "h2d_A", r))) return s;
     TB_CUDA(cudaEventRecord(evA[r], hs), "event record");
   }
   // Phase 1: panel p of every row group once it has landed; row group g
@@ -906,6 +998,9 @@ void tb_release(void) {
       for (cudaEvent_t e : pool) cudaEventDestroy(e);
       pool.clear();
     }
+    for (auto& kv : st.stage_ws)
+      if (kv.second.buf) cudaFree(kv.second.buf);
+    st.stage_ws.clear();
     for (auto& kv : st.split_ws) {
       if (kv.second.partials) cudaFree(kv.second.partials);
       if (kv.second.counters) cudaFree(kv.second.counters);

@@ -353,6 +353,60 @@ def test_flat_pipeline_shapes(tb, oracle, monkeypatch, shape):
     assert (torch.linalg.norm(got - ref) / torch.linalg.norm(ref)).item() <= NORMWISE
 
 
+def test_staged_tma_for_misaligned_operands(tb, oracle):
+    """AUTO on operands TMA cannot address (odd leading dimension; base off a
+    16-byte boundary) above the staging threshold copies them to even-pitch
+    workspace and runs the TMA kernel: results equal the oracle's rows and
+    cuBLAS normwise; the caller's buffers are untouched."""
+    import torch
+
+    m = k = n = 2223  # odd: lda = ldb = 2223; 2.2e10 flops >= the staging threshold
+    a, b = oracle.generate(m, k, 31), oracle.generate(k, n, 32)
+    ta, tbm = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    c, sec = tb.dgemm(ta, tbm)
+    rows = np.arange(0, m, 97)
+    want = oracle.tiled_parallel(a[rows], b)
+    assert oracle.normwise_rel(c.cpu().numpy()[rows], want) <= NORMWISE
+    assert torch.equal(ta.cpu(), torch.from_numpy(a))
+    # even leading dims, but the bases are 8 bytes past a 16-byte boundary (column views)
+    big_a = torch.from_numpy(oracle.generate(m, k + 3, 33)).cuda()
+    big_b = torch.from_numpy(oracle.generate(k, n + 3, 34)).cuda()
+    va, vb = big_a[:, 1:k + 1], big_b[:, 1:n + 1]
+    assert va.stride(0) % 2 == 0 and (va.data_ptr() % 16) == 8
+    out = torch.empty((m, n), dtype=torch.float64, device="cuda")
+    tb.dgemm_launch(va, vb, out)
+    ref, _ = tb.cublas_dgemm(va.contiguous(), vb.contiguous())
+    torch.cuda.synchronize()
+    assert (torch.linalg.norm(out - ref) / torch.linalg.norm(ref)).item() <= NORMWISE
+
+
+def test_concurrent_host_threads(tb, oracle):
+    """The registered MultiplyFn and the flat host entry called from several
+    host threads at once (the reference's CPU backends are thread-safe,
+    test_backends.py:136-149; the GPU library serialises per device)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    shapes = [(300, 200, 100), (129, 257, 65), (640, 64, 512), (1000, 300, 700)] * 2
+    ops = [(oracle.generate(m, k, 20 + i), oracle.generate(k, n, 40 + i)) for i, (m, k, n) in enumerate(shapes)]
+
+    def via_fn(i):
+        a, b = ops[i]
+        return tb.gpu_tiled_multiply(a, b)
+
+    def via_flat(i):
+        a, b = ops[i]
+        c = np.zeros(a.shape[0] * b.shape[1])
+        assert tb.gpu_tiled_multiply_flat(0, a, b, a.shape[0], a.shape[1], b.shape[1], 32, c,
+                                          np.zeros(1)) == tb.STATUS_OK
+        return c.reshape(a.shape[0], b.shape[1])
+
+    with ThreadPoolExecutor(max_workers=4) as ex:
+        futs = [ex.submit(via_fn if i % 2 else via_flat, i) for i in range(len(ops))]
+        for i, f in enumerate(futs):
+            a, b = ops[i]
+            assert oracle.normwise_rel(f.result(), oracle.tiled_parallel(a, b)) <= NORMWISE
+
+
 def test_cli_run_writes_reference_csv(tb, tmp_path):
     from paper_2509_04594_b200.__main__ import main
 

@@ -40,8 +40,12 @@ enum class Loader : int { TMA = 0, CPASYNC = 1 };
 // DFMA (scalar fused multiply-add, 8x8 register tile per thread).
 enum class Math : int { DMMA = 0, DFMA = 1 };
 
-struct DmmaCfg {
-  static constexpr int BM = 128, BN = 128, BK = 16;
+// BM (tile rows) is a template parameter: 128 is the production tile; 64
+// halves the row padding and doubles the tile count for small problems
+// (warp tile 32 x 32). Everything else is shared.
+template <int BM_>
+struct DmmaCfgT {
+  static constexpr int BM = BM_, BN = 128, BK = 16;
   static constexpr int WARPS_M = 2, WARPS_N = 4;
   static constexpr int WM = BM / WARPS_M;  // 64
   static constexpr int WN = BN / WARPS_N;  // 32
@@ -63,11 +67,12 @@ struct DmmaCfg {
   static constexpr int GROUP_M = 8;          // tile raster: GROUP_M tile-rows per band
   static constexpr int TILE_ELEMS = BM * BN;
 };
+using DmmaCfg = DmmaCfgT<128>;
 
-// A pipeline stage holds SUB consecutive 16-deep k sub-slabs (SUB * 32 KB).
-template <int SUB, int STAGES>
+// A pipeline stage holds SUB consecutive 16-deep k sub-slabs (SUB * STAGE bytes).
+template <int SUB, int STAGES, int BM = 128>
 constexpr int dmma_smem_bytes() {
-  return STAGES * SUB * DmmaCfg::STAGE + 2 * STAGES * 8 + 16 + 1024;  // + barriers + flag + alignment slack
+  return STAGES * SUB * DmmaCfgT<BM>::STAGE + 2 * STAGES * 8 + 16 + 1024;  // + barriers + flag + alignment slack
 }
 
 struct GemmParams {
@@ -144,11 +149,12 @@ struct WorkIter {
 
 __device__ __forceinline__ void consumer_bar() { asm volatile("bar.sync 1, %0;\n" ::"n"(DmmaCfg::CONSUMER_THREADS)); }
 
-template <int SUB, int STAGES, Loader LD, Math MT = Math::DMMA>
+template <int SUB, int STAGES, Loader LD, Math MT = Math::DMMA, int BM = 128>
 __global__ void __launch_bounds__(DmmaCfg::THREADS, 1)
     dgemm_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       const GemmParams p) {
-  using C = DmmaCfg;
+  using C = DmmaCfgT<BM>;
+  static_assert(MT == Math::DMMA || BM == 128, "the DFMA comparison path is laid out for 128-row tiles");
   extern __shared__ uint8_t smem_raw[];
   // SWIZZLE_128B's XOR pattern is a function of absolute smem address bits
   // [4:6] ^ [7:9]: stage buffers must start on 1024-byte boundaries.

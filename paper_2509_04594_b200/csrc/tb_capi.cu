@@ -72,6 +72,39 @@ int cfg_smem(int idx) {
     default: return KernelSet<1, 6>::smem();
   }
 }
+
+// 64-row tiles for small problems (DmmaCfgT<64>): 24 KB stages, 8 deep.
+constexpr int kSmallStages = 8;
+void* small_kernel(bool tma) {
+  return tma ? (void*)tb::dgemm_dmma_kernel<1, kSmallStages, tb::Loader::TMA, tb::Math::DMMA, 64>
+             : (void*)tb::dgemm_dmma_kernel<1, kSmallStages, tb::Loader::CPASYNC, tb::Math::DMMA, 64>;
+}
+constexpr int small_smem() { return tb::dmma_smem_bytes<1, kSmallStages, 64>(); }
+
+// Tile rows for a DMMA launch (measured, profiles/r01_bm_ab.txt). 64-row
+// tiles run ~2 % less efficiently per flop than 128-row tiles (warp tile
+// 32 x 32: more fragment loads per DMMA) but double the tile count and can
+// halve the row padding:
+//  - fewer than two waves of 128-row tiles (and not a >= 90 % single wave,
+//    which runs data-parallel): 64 rows — parallelism wins (N = 600 / 1000 /
+//    1200 / 1700 / 2000: +33 / +10 / +14 / +5 / +1 %);
+//  - otherwise 64 rows only if its padded row count, weighted by that 2 %,
+//    is smaller (N = 2223 / 3000 take 64; 4000 / 5000 / 8000 / 10000 and the
+//    1250-row shard keep 128).
+// TB_BM=64|128 forces (A/B experiments).
+int choose_bm(int64_t m, int64_t n, int sms, bool dfma) {
+  static const int forced = [] {
+    const char* e = std::getenv("TB_BM");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (dfma) return 128;
+  if (forced == 64 || forced == 128) return forced;
+  const int64_t t128 = ((m + 127) / 128) * ((n + 127) / 128);
+  const bool dp_wave = t128 < sms && 10 * t128 >= 9 * (int64_t)sms;
+  if (t128 < 2 * (int64_t)sms && !dp_wave) return 64;
+  const double rows64 = (double)((m + 63) / 64 * 64) * 1.021, rows128 = (double)((m + 127) / 128 * 128);
+  return rows64 < rows128 ? 64 : 128;
+}
 constexpr int kMaxDevices = 64;
 constexpr int kMaxBlockThreads = 1024;     // limits.ts:20-24 maxThreadsPerBlock
 
@@ -176,6 +209,10 @@ int ensure_kernel_attrs(int dev) {
     TB_CUDA(cudaFuncSetAttribute(cfg_kernel(i, false), cudaFuncAttributeMaxDynamicSharedMemorySize, cfg_smem(i)),
             "set smem attribute (dmma_cpasync)");
   }
+  if (small_smem() <= st.smem_optin)
+    for (bool tma : {true, false})
+      TB_CUDA(cudaFuncSetAttribute(small_kernel(tma), cudaFuncAttributeMaxDynamicSharedMemorySize, small_smem()),
+              "set smem attribute (64-row tiles)");
   TB_CUDA(cudaFuncSetAttribute(tb::dgemm_paper_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                st.smem_optin),
           "set smem attribute (paper)");
@@ -485,7 +522,9 @@ int launch(int dev, const double* A, int64_t lda, const double* B, int64_t ldb, 
     p.m = (int)m;
     p.n = (int)n;
     p.k = (int)k;
-    p.tiles_m = (int)((m + Cfg::BM - 1) / Cfg::BM);
+    const bool dfma = variant == TB_VARIANT_DFMA;
+    const int bm = choose_bm(m, n, g_dev[dev].sms, dfma);
+    p.tiles_m = (int)((m + bm - 1) / bm);
     p.tiles_n = (int)((n + Cfg::BN - 1) / Cfg::BN);
     p.accumulate = accumulate;
     p.vec_store = ((reinterpret_cast<uintptr_t>(Cm) & 15u) == 0 && ldc % 2 == 0) ? 1 : 0;
@@ -494,9 +533,8 @@ int launch(int dev, const double* A, int64_t lda, const double* B, int64_t ldb, 
       set_err("too many output tiles");
       return TB_STATUS_OVER_LIMITS;
     }
-    const bool dfma = variant == TB_VARIANT_DFMA;
     const int cfg = dfma ? 0 : active_cfg();
-    const int64_t kstage = (int64_t)Cfg::BK * kCfgs[cfg].sub;
+    const int64_t kstage = bm == 64 ? (int64_t)Cfg::BK : (int64_t)Cfg::BK * kCfgs[cfg].sub;
     p.num_k = (int)((k + kstage - 1) / kstage);
     const Schedule sc = plan_schedule(tiles, p.num_k, g_dev[dev].sms);
     p.num_k = sc.num_k;  // split-K pads the k-slab count (extra slabs read as zeros)
@@ -525,12 +563,13 @@ int launch(int dev, const double* A, int64_t lda, const double* B, int64_t ldb, 
     const bool use_tma = variant == TB_VARIANT_DMMA_TMA || (dfma && tma_ok(A, lda, B, ldb));
     if (use_tma) {
       if ((s = get_encoder())) return s;
-      if ((s = encode_map(&mA, A, m, k, lda, Cfg::BM))) return s;
+      if ((s = encode_map(&mA, A, m, k, lda, (uint32_t)bm))) return s;
       if ((s = encode_map(&mB, B, k, n, ldb, Cfg::BK))) return s;
     }
     void* args[] = {&mA, &mB, &p};
-    TB_CUDA(cudaLaunchKernel(cfg_kernel(cfg, use_tma, dfma), dim3((unsigned)sc.grid), dim3(Cfg::THREADS), args,
-                             (size_t)cfg_smem(cfg), stream),
+    TB_CUDA(cudaLaunchKernel(bm == 64 ? small_kernel(use_tma) : cfg_kernel(cfg, use_tma, dfma),
+                             dim3((unsigned)sc.grid), dim3(Cfg::THREADS), args,
+                             (size_t)(bm == 64 ? small_smem() : cfg_smem(cfg)), stream),
             "kernel launch");
 #ifdef TB_TIMELINE
     if (tl_buf) {

@@ -317,6 +317,58 @@ __global__ void __launch_bounds__(DmmaCfg::THREADS, 1)
       for (int j = 0; j < C::NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
     TB_TL(unsigned long long tl_u = 0;)
+    if constexpr (MT == Math::DMMA && SUB == 1 && BM == 128) {
+      // Cross-stage fragment prefetch: the next stage's full barrier is
+      // waited on, and its first half-step fragments loaded, before this
+      // stage's second half-step DMMAs issue, so the tensor pipe does not
+      // drain at stage boundaries (+0.3-0.45 % at N = 5000-10000 and on the
+      // 1250-row shard, profiles/r01_xpf_ab.txt; a few address registers
+      // spill, per stage, outside the DMMA stream). The 64-row tiles keep
+      // the plain loop below (measured neutral to -0.3 % there).
+      double2 fa[2][C::MI];
+      double fb[2][2][C::NI];
+      auto ld = [&](int stage, int half, int buf) {
+        const uint8_t* sa = smem + stage * STAGE_BYTES;
+        const uint8_t* sb = sa + C::A_STAGE;
+#pragma unroll
+        for (int i = 0; i < C::MI; ++i)
+          fa[buf][i] = *reinterpret_cast<const double2*>(sa + (half ? a_off1 : a_off0) + i * 8 * 128);
+#pragma unroll
+        for (int j = 0; j < C::NI; ++j) {
+          const uint32_t box = (j >> 1) * C::B_BOX, flip = (j & 1) ? 64u : 0u;
+          fb[buf][0][j] = *reinterpret_cast<const double*>(sb + box + (b_off[2 * half] ^ flip));
+          fb[buf][1][j] = *reinterpret_cast<const double*>(sb + box + (b_off[2 * half + 1] ^ flip));
+        }
+      };
+      auto mma = [&](int buf) {
+#pragma unroll
+        for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+          for (int j = 0; j < C::NI; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], fa[buf][i].x, fb[buf][0][j]);
+#pragma unroll
+        for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+          for (int j = 0; j < C::NI; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], fa[buf][i].y, fb[buf][1][j]);
+      };
+      mbar_wait(smem_u32(&full[s]), ph);
+      ld(s, 0, 0);
+      for (int kt = kb; kt < ke; ++kt) {
+        ld(s, 1, 1);
+        mma(0);
+        const int s1 = s + 1 == STAGES ? 0 : s + 1;
+        const uint32_t ph1 = s + 1 == STAGES ? ph ^ 1 : ph;
+        if (kt + 1 < ke) {
+          mbar_wait(smem_u32(&full[s1]), ph1);
+          ld(s1, 0, 0);
+        }
+        mma(1);
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&empty[s]));
+        s = s1;
+        ph = ph1;
+      }
+    } else
     for (int kt = kb; kt < ke; ++kt) {
       mbar_wait(smem_u32(&full[s]), ph);
       TB_TL(if (tl && ct == 0 && kt == kb) { tl_u = tl_now(); if (tl[1] == 0) tl[1] = tl_u; })

@@ -100,7 +100,7 @@ int choose_bm(int64_t m, int64_t n, int sms, bool dfma) {
   if (dfma) return 128;
   if (forced == 64 || forced == 128) return forced;
   const int64_t t128 = ((m + 127) / 128) * ((n + 127) / 128);
-  const bool dp_wave = t128 < sms && 10 * t128 >= 9 * (int64_t)sms;
+  const bool dp_wave = t128 < sms && 10 * t128 >= 9 * (int64_t)sms;  // 128-row DP wave (N = 1500)
   if (t128 < 2 * (int64_t)sms && !dp_wave) return 64;
   const double rows64 = (double)((m + 63) / 64 * 64) * 1.021, rows128 = (double)((m + 127) / 128 * 128);
   return rows64 < rows128 ? 64 : 128;
@@ -328,7 +328,7 @@ int check_device(int32_t device) {
 // the CTAs, then a stream-K region whose k-iterations are split evenly across
 // them. Three shapes, chosen on the host (the kernel is the same):
 //  - stream-K: the last (T mod P) + P tiles split over P = #SM CTAs;
-//  - data-parallel: no split when a single wave is >= 90 % full — splitting
+//  - data-parallel: no split when a single wave is >= 75 % full — splitting
 //    every tile costs partial-tile traffic and fixups that an idle 10 % does
 //    not (measured: with several waves the stream-K tail still wins);
 //  - split-K: T <= P/2 tiles each split into exactly s = P / T equal k-ranges
@@ -351,9 +351,12 @@ Schedule plan_schedule(int64_t tiles, int num_k, int sms) {
   Schedule sc{sms, (int)tiles, 0, 1, 1, num_k};
   const int64_t rem = tiles % sms;
   if (forced == 1 || rem == 0) return sc;
-  // A single wave >= 90 % full runs data-parallel (N = 1500: 144 tiles, 28.6 -> 31.2 TFLOP/s); with
-  // more waves the stream-K tail stays ahead (N = 4000 / 6000 at 92 %: 34.12 / 35.84 vs 33.99 / 35.76).
-  if (forced == 0 && tiles < sms && 10 * tiles >= 9 * sms) return sc;
+  // A single wave >= 75 % full runs data-parallel: splitting every tile of a single wave costs about a
+  // quarter of a tile's k-loop in partial traffic and fixups (N = 1500, 144 tiles: 28.6 -> 31.2;
+  // N = 1000 on 64-row tiles, 128 tiles: 23.3 -> 25.9; N = 900, 120 tiles: 19.5 -> 20.5; at 61 %,
+  // N = 800, stream-K stays ahead 18.2 vs 15.9 TFLOP/s). With more waves the stream-K tail wins
+  // (N = 4000 / 6000 at 92 %: 34.12 / 35.84 vs 33.99 / 35.76).
+  if (forced == 0 && tiles < sms && 4 * tiles >= 3 * sms) return sc;
   const int64_t min_seg = num_k < 8 ? num_k : 8;      // keep segments long enough to amortise the fixup
   if (forced == 0 && 2 * tiles <= sms) {
     int64_t split = std::min<int64_t>(sms / tiles, num_k / min_seg);

@@ -30,6 +30,7 @@
 // conflict-free 64-bit loads (derivation in DESIGN.md §4).
 #pragma once
 #include <cstdint>
+#include <type_traits>
 #include <cuda.h>
 #include "ptx.cuh"
 
@@ -96,6 +97,20 @@ struct GemmParams {
   unsigned long long* timeline;  // tooling build only: [grid][8] per-CTA %globaltimer stamps
 #endif
 };
+// Pipelined host-buffer mode (PIPE instantiation only) has no stream-K
+// region, so it reuses the stream-K fields (keeping GemmParams' layout, which
+// ptxas's allocation for the production kernel turned out to depend on):
+//   sk_tiles  -> number of K-panels Q
+//   counters  -> panel_it[Q + 1]: panel q covers k-stages [panel_it[q], panel_it[q+1])
+//   partials  -> panel_flags[Q] (int): panel q is usable once its flag != 0
+//                (written by the copy stream after the panel's copies).
+// Each CTA owns tiles blockIdx.x, +gridDim.x, ... and walks them
+// panel-major, accumulating into C for panels after the first.
+__device__ __forceinline__ int pipe_panels(const GemmParams& p) { return p.sk_tiles; }
+__device__ __forceinline__ const int* pipe_panel_it(const GemmParams& p) { return p.counters; }
+__device__ __forceinline__ const int* pipe_flags(const GemmParams& p) {
+  return reinterpret_cast<const int*>(p.partials);
+}
 
 #ifdef TB_TIMELINE
 __device__ __forceinline__ unsigned long long tl_now() {
@@ -147,13 +162,34 @@ struct WorkIter {
   }
 };
 
+// PIPE mode work list: (tile, panel) units, panel-major over this CTA's tiles.
+struct PipeIter {
+  int t, q;
+  __device__ __forceinline__ explicit PipeIter(const GemmParams&) : t(blockIdx.x), q(0) {}
+  __device__ __forceinline__ bool next(const GemmParams& p, int& tile, int& kb, int& ke) {
+    const int tiles = p.tiles_m * p.tiles_n;
+    if (t >= tiles) {
+      t = blockIdx.x;
+      ++q;
+    }
+    if (q >= pipe_panels(p) || t >= tiles) return false;
+    tile = t;
+    kb = pipe_panel_it(p)[q];
+    ke = pipe_panel_it(p)[q + 1];
+    t += gridDim.x;
+    return true;
+  }
+};
+
 __device__ __forceinline__ void consumer_bar() { asm volatile("bar.sync 1, %0;\n" ::"n"(DmmaCfg::CONSUMER_THREADS)); }
 
-template <int SUB, int STAGES, Loader LD, Math MT = Math::DMMA, int BM = 128>
+template <int SUB, int STAGES, Loader LD, Math MT = Math::DMMA, int BM = 128, bool PIPE = false>
 __global__ void __launch_bounds__(DmmaCfg::THREADS, 1)
     dgemm_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       const GemmParams p) {
   using C = DmmaCfgT<BM>;
+  using Iter = typename std::conditional<PIPE, PipeIter, WorkIter>::type;
+  static_assert(!PIPE || (LD == Loader::TMA && MT == Math::DMMA), "PIPE mode: TMA + DMMA only");
   static_assert(MT == Math::DMMA || BM == 128, "the DFMA comparison path is laid out for 128-row tiles");
   extern __shared__ uint8_t smem_raw[];
   // SWIZZLE_128B's XOR pattern is a function of absolute smem address bits
@@ -196,9 +232,23 @@ __global__ void __launch_bounds__(DmmaCfg::THREADS, 1)
     // wait that could depend on it (no deadlock).
     constexpr int CP_LAG = STAGES - 1 < 4 ? STAGES - 1 : 4;
     int g = 0;
-    WorkIter w(p);
+    Iter w(p);
     int tile, kb, ke;
+    int ready_upto = 0;  // PIPE: panel flags observed set so far
     while (w.next(p, tile, kb, ke)) {
+      if constexpr (PIPE) {
+        // Wait for the panel holding k-stages [kb, ke) (panels land in order).
+        while (ready_upto < pipe_panels(p) && pipe_panel_it(p)[ready_upto] <= kb) {
+          if (ld_acquire_gpu(&pipe_flags(p)[ready_upto]) == 0) {
+            // Bounded: a panel that never lands (a broken host pipeline)
+            // faults the launch after ~10 s instead of hanging the device.
+            const unsigned long long t_start = globaltimer_ns();
+            while (ld_acquire_gpu(&pipe_flags(p)[ready_upto]) == 0)
+              if (globaltimer_ns() - t_start > 10000000000ull) __trap();
+          }
+          ++ready_upto;
+        }
+      }
       int tm, tn;
       tile_coords(tile, p.tiles_m, p.tiles_n, tm, tn);
       const int m0 = tm * C::BM, n0 = tn * C::BN;
@@ -307,7 +357,7 @@ __global__ void __launch_bounds__(DmmaCfg::THREADS, 1)
 
   int s = 0;
   uint32_t ph = 0;
-  WorkIter w(p);
+  Iter w(p);
   int tile, kb, ke;
   while (w.next(p, tile, kb, ke)) {
     double acc[C::MI][C::NI][2];
@@ -450,7 +500,7 @@ __global__ void __launch_bounds__(DmmaCfg::THREADS, 1)
     TB_TL(const unsigned long long tl_m = tl && ct == 0 ? tl_now() : 0;)
     TB_TL(if (tl && ct == 0) { tl[2] = tl_m; tl[4] += 1; tl[7] += tl_m - tl_u; })
     // ------------------------------------------------- stream-K segment fixup
-    if (kb != 0 || ke != p.num_k) {
+    if (!PIPE && (kb != 0 || ke != p.num_k)) {
       const int st = tile - p.dp_tiles;
       const int64_t first = (int64_t)st * p.num_k;
       const int seg = (int)((first + kb) / p.sk_ipc - first / p.sk_ipc);
@@ -498,7 +548,9 @@ __global__ void __launch_bounds__(DmmaCfg::THREADS, 1)
     int tm, tn;
     tile_coords(tile, p.tiles_m, p.tiles_n, tm, tn);
     const int m0 = tm * C::BM, n0 = tn * C::BN;
-    if (p.accumulate && p.vec_store && m0 + C::BM <= p.m && n0 + C::BN <= p.n) {
+    // C += A·B when asked; in PIPE mode also for every panel after the first.
+#define TB_ACCUM (PIPE ? (p.accumulate || kb != 0) : p.accumulate)
+    if (TB_ACCUM && p.vec_store && m0 + C::BM <= p.m && n0 + C::BN <= p.n) {
       // C += A·B on an interior tile: the old C values are fetched in two
       // batches of 16 independent 16-byte loads (no branches, no stores in
       // between), so the epilogue pays two memory round trips, not one per
@@ -521,7 +573,8 @@ __global__ void __launch_bounds__(DmmaCfg::THREADS, 1)
             acc[h * C::MI / 2 + ii][j][1] += old[ii][j].y;
           }
       }
-    } else if (p.accumulate) {
+    } else if (TB_ACCUM) {
+#undef TB_ACCUM
       // Edge tiles / unaligned rows: element-wise, bounds-checked.
 #pragma unroll
       for (int i = 0; i < C::MI; ++i) {

@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstring>
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <vector>
 #include <map>
@@ -80,6 +81,9 @@ void* small_kernel(bool tma) {
              : (void*)tb::dgemm_dmma_kernel<1, kSmallStages, tb::Loader::CPASYNC, tb::Math::DMMA, 64>;
 }
 constexpr int small_smem() { return tb::dmma_smem_bytes<1, kSmallStages, 64>(); }
+
+// The host pipeline's fused phase-1 kernel (PIPE mode, dgemm_dmma.cuh).
+void* pipe_kernel() { return (void*)tb::dgemm_dmma_kernel<1, 6, tb::Loader::TMA, tb::Math::DMMA, 128, true>; }
 
 // Tile rows for a DMMA launch (measured, profiles/r01_bm_ab.txt). 64-row
 // tiles run ~2 % less efficiently per flop than 128-row tiles (warp tile
@@ -155,6 +159,8 @@ struct DeviceState {
   };
   std::map<cudaStream_t, StageWs> stage_ws;
   std::vector<cudaEvent_t> ev_pool[2];  // host-buffer entry: [timing, no-timing] events
+  int* dtab = nullptr;                  // host-buffer entry: [0,128) panel flags, [128,256) panel k-stages
+  int* htab = nullptr;                  // pinned: [0,128) zeros, [128,256) panel k-stages, [256] = 1
 };
 
 DeviceState g_dev[kMaxDevices];
@@ -209,6 +215,9 @@ int ensure_kernel_attrs(int dev) {
     TB_CUDA(cudaFuncSetAttribute(cfg_kernel(i, false), cudaFuncAttributeMaxDynamicSharedMemorySize, cfg_smem(i)),
             "set smem attribute (dmma_cpasync)");
   }
+  if (cfg_smem(0) <= st.smem_optin)
+    TB_CUDA(cudaFuncSetAttribute(pipe_kernel(), cudaFuncAttributeMaxDynamicSharedMemorySize, cfg_smem(0)),
+            "set smem attribute (pipe)");
   if (small_smem() <= st.smem_optin)
     for (bool tma : {true, false})
       TB_CUDA(cudaFuncSetAttribute(small_kernel(tma), cudaFuncAttributeMaxDynamicSharedMemorySize, small_smem()),
@@ -615,6 +624,50 @@ int launch(int dev, const double* A, int64_t lda, const double* B, int64_t ldb, 
   return TB_STATUS_OK;
 }
 
+// One persistent launch for the host pipeline's phase 1 (PIPE mode): C =
+// A·B over all k, k-panel q (k-stages [panel_it[q], panel_it[q+1]), panel_it
+// in device memory) consumed once flags[q] != 0. TMA operands (even pitch,
+// 16-byte aligned) only.
+int launch_pipe(int dev, const double* A, int64_t lda, const double* B, int64_t ldb, double* Cm, int64_t ldc,
+                int64_t m, int64_t k, int64_t n, const int* panel_it_d, const int* flags_d, int Q,
+                cudaStream_t stream) {
+  int s = ensure_kernel_attrs(dev);
+  if (s) return s;
+  using Cfg = tb::DmmaCfg;
+  tb::GemmParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.A = A;
+  p.B = B;
+  p.C = Cm;
+  p.lda = lda;
+  p.ldb = ldb;
+  p.ldc = ldc;
+  p.m = (int)m;
+  p.n = (int)n;
+  p.k = (int)k;
+  p.tiles_m = (int)((m + Cfg::BM - 1) / Cfg::BM);
+  p.tiles_n = (int)((n + Cfg::BN - 1) / Cfg::BN);
+  p.num_k = (int)((k + Cfg::BK - 1) / Cfg::BK);
+  p.accumulate = 0;
+  p.vec_store = ((reinterpret_cast<uintptr_t>(Cm) & 15u) == 0 && ldc % 2 == 0) ? 1 : 0;
+  const int64_t tiles = (int64_t)p.tiles_m * p.tiles_n;
+  p.dp_tiles = (int)tiles;
+  p.sk_tiles = Q;                                        // PIPE: panel count
+  p.sk_ipc = 1;
+  p.max_seg = 1;
+  p.counters = const_cast<int*>(panel_it_d);             // PIPE: panel k-stage bounds
+  p.partials = reinterpret_cast<double*>(const_cast<int*>(flags_d));  // PIPE: panel flags
+  if ((s = get_encoder())) return s;
+  CUtensorMap mA, mB;
+  if ((s = encode_map(&mA, A, m, k, lda, Cfg::BM))) return s;
+  if ((s = encode_map(&mB, B, k, n, ldb, Cfg::BK))) return s;
+  void* args[] = {&mA, &mB, &p};
+  const int grid = (int)std::min<int64_t>(tiles, g_dev[dev].sms);
+  TB_CUDA(cudaLaunchKernel(pipe_kernel(), dim3((unsigned)grid), dim3(Cfg::THREADS), args, (size_t)cfg_smem(0), stream),
+          "kernel launch (pipe)");
+  return TB_STATUS_OK;
+}
+
 struct EventPair {
   cudaEvent_t a = nullptr, b = nullptr;
   ~EventPair() {
@@ -791,6 +844,7 @@ int tb_gpu_tiled_multiply_flat_ex(int32_t device, const double* a, const double*
   //  once, and the last blocks shrink so the final D2H is short.
   // Small problems degenerate to copy, GEMM, copy.
   int64_t Mq = m;
+  bool fused = false;             // phase 1 as one PIPE-mode launch
   std::vector<int64_t> pk{0, k};  // phase-1 K-panel bounds
   std::vector<int64_t> gb{0, m};  // phase-1 row groups (one per compute stream)
   std::vector<int64_t> rb{m};     // phase-2 row-block bounds, rb[0] = Mq
@@ -813,7 +867,33 @@ int tb_gpu_tiled_multiply_flat_ex(int32_t device, const double* a, const double*
       }
     }
     mq = (mq + 127) / 128 * 128;
+    // Phase 1 as one persistent launch that waits on per-panel flags (PIPE
+    // mode) rather than a launch per panel and row group; TB_PIPE_FUSED=0
+    // restores the launch-per-panel form (A/B).
+    static const bool fused_env = !(std::getenv("TB_PIPE_FUSED") && std::strcmp(std::getenv("TB_PIPE_FUSED"), "0") == 0);
+    fused = fused_env && variant != TB_VARIANT_PAPER && variant != TB_VARIANT_DFMA &&
+            variant != TB_VARIANT_DMMA_CPASYNC && cfg_smem(0) <= g_dev[device].smem_optin;
+    if (fused && !std::getenv("TB_PIPE")) {
+      // The fused launch gives CTA c the phase-1 tiles c, c + P, ...: pick
+      // the tile-row count (>= the compute-cover minimum, up to 8 more) whose
+      // tile count leaves the least imbalance, ceil(T/P) - T/P (N = 10000:
+      // 34 rows -> 18.15 tiles per CTA, 59.1 ms; 41 rows -> 21.89, 58.0 ms;
+      // profiles/r01_pipe_trace_mq_sweep.txt).
+      const int64_t tn = (n + 127) / 128, P_sm = g_dev[device].sms;
+      int64_t best_r = mq / 128;
+      double best_imb = 2.0;
+      for (int64_t rr = mq / 128; rr <= mq / 128 + 8 && rr * 128 < m - blk / 2; ++rr) {
+        const double per = (double)(rr * tn) / (double)P_sm;
+        const double imb = std::ceil(per) - per;
+        if (imb < best_imb - 1e-9) {
+          best_imb = imb;
+          best_r = rr;
+        }
+      }
+      mq = best_r * 128;
+    }
     Mq = mq >= m - blk / 2 ? m : mq;
+    const int64_t kal = fused ? 16 : 2;  // panel bounds on k-stage (PIPE) or TMA (even k0) boundaries
     // Panel sizes: after a small first panel, each panel is as large as can
     // land (transfer model) before the GEMMs queued so far drain (compute
     // model), so the panels grow geometrically by the compute/transfer ratio
@@ -822,7 +902,8 @@ int tb_gpu_tiled_multiply_flat_ex(int32_t device, const double* a, const double*
     pk.assign(1, 0);
     double arrive = 0.0, finish = 0.0;
     for (int64_t at = 0, step = kp0; at < k;) {
-      int64_t nx = at + step >= k - step / 2 ? k : ((at + step) & ~int64_t(1));  // even k0: TMA alignment
+      int64_t nx = at + step >= k - step / 2 ? k : ((at + step) / kal * kal);
+      if (nx <= at) nx = std::min<int64_t>(k, at + kal);
       arrive += tr_per_k * (double)(nx - at);
       finish = std::max(finish, arrive) + c_per_k * (double)(nx - at);
       pk.push_back(nx);
@@ -840,10 +921,14 @@ int tb_gpu_tiled_multiply_flat_ex(int32_t device, const double* a, const double*
       }
     rb.assign(1, Mq);
     const int64_t nb = (r + blk - 1) / blk;
-    for (int64_t i = 1; i <= nb; ++i) rb.push_back(Mq + r * i / nb);
+    // Block bounds on 128-row tile boundaries: a block of, say, 1413 rows
+    // would pad its last tile row to 1536 (8 % of its DMMAs on zeros).
+    for (int64_t i = 1; i <= nb; ++i)
+      rb.push_back(i == nb ? Mq + r : std::min(Mq + r, Mq + (r * i / nb + 64) / 128 * 128));
     for (auto it = tail.rbegin(); it != tail.rend(); ++it) rb.push_back(rb.back() + *it);
   }
   const int P = (int)pk.size() - 1, G = (int)gb.size() - 1, R = (int)rb.size() - 1;
+  if (P < 2 || P > 120) fused = false;
 
   // Events come from a per-device pool reused across calls (every call
   // drains its streams before returning), so the host does not create and
@@ -945,27 +1030,63 @@ int tb_gpu_tiled_multiply_flat_ex(int32_t device, const double* a, const double*
   TB_CUDA(cudaEventRecord(e_start, hs), "event record");
   for (cudaStream_t cs : css) TB_CUDA(cudaStreamWaitEvent(cs, e_start, 0), "stream wait");
   TB_CUDA(cudaStreamWaitEvent(ds, e_start, 0), "stream wait");
-  // H2D: phase-1 panels (A slice, then B rows), then the phase-2 row blocks.
+  cudaEvent_t evTab = nullptr;
+  if (fused) {
+    // PIPE tables: flags zeroed and panel k-stage bounds uploaded on the copy
+    // stream (copy engine, no SM: the phase-1 kernel may occupy every SM).
+    if (!st.dtab) {
+      TB_CUDA(cudaMalloc(&st.dtab, 512 * sizeof(int)), "pipeline table allocation");
+      TB_CUDA(cudaHostAlloc(&st.htab, 512 * sizeof(int), cudaHostAllocDefault), "pipeline table allocation");
+      std::memset(st.htab, 0, 512 * sizeof(int));
+      st.htab[256] = 1;
+    }
+    for (int q = 0; q <= P; ++q) st.htab[128 + q] = (int)((pk[q] + 15) / 16);
+    TB_CUDA(cudaMemcpyAsync(st.dtab, st.htab, (size_t)P * sizeof(int), cudaMemcpyHostToDevice, hs), "flags reset");
+    TB_CUDA(cudaMemcpyAsync(st.dtab + 128, st.htab + 128, (size_t)(P + 1) * sizeof(int), cudaMemcpyHostToDevice, hs),
+            "panel table");
+    if (!(evTab = mk(cudaEventDisableTiming))) return cuda_fail(cudaGetLastError(), "event create");
+    TB_CUDA(cudaEventRecord(evTab, hs), "event record");
+  }
+  // H2D: phase-1 panels (A slice, then B rows; in fused mode then the
+  // panel's flag, copied after its data on the same stream), then the
+  // phase-2 row blocks.
   for (int p = 0; p < P; ++p) {
     if (Mq > 0 && (s = h2d(dA, lda_d, a, k, 0, Mq, pk[p], pk[p + 1], "h2d_Ap", p))) return s;
     if ((s = h2d(dB, ldb_d, b, n, pk[p], pk[p + 1], 0, n, "h2d_Bp", p))) return s;
     TB_CUDA(cudaEventRecord(evP[p], hs), "event record");
+    if (fused)
+      TB_CUDA(cudaMemcpyAsync(st.dtab + p, st.htab + 256, sizeof(int), cudaMemcpyHostToDevice, hs), "panel flag");
   }
   for (int r = 0; r < R; ++r) {
     if ((s = h2d(dA, lda_d, a, k, rb[r], rb[r + 1], 0, k, "h2d_A", r))) return s;
     TB_CUDA(cudaEventRecord(evA[r], hs), "event record");
   }
-  // Phase 1: panel p of every row group once it has landed; row group g
-  // stays on stream g, so its partial sums accumulate in panel order.
-  for (int p = 0; p < P; ++p)
-    for (int g = 0; g < G; ++g) {
-      TB_CUDA(cudaStreamWaitEvent(css[g], evP[p], 0), "stream wait");
-      if ((s = gemm(css[g], gb[g], gb[g + 1], pk[p], pk[p + 1], p > 0))) return s;
-      if (p == P - 1 && (s = d2h(css[g], gb[g], gb[g + 1]))) return s;
-    }
-  // Phase 2: full-K row blocks, alternating streams.
+  if (fused) {
+    // Phase 1: one persistent launch; its producer waits on each panel's flag.
+    const cudaStream_t cs = css[0];
+    TB_CUDA(cudaStreamWaitEvent(cs, evTab, 0), "stream wait");
+    cudaEvent_t t0 = mk(cudaEventDefault), t1 = mk(cudaEventDefault);
+    if (!t0 || !t1) return cuda_fail(cudaGetLastError(), "event create");
+    kt0.push_back(t0);
+    kt1.push_back(t1);
+    TB_CUDA(cudaEventRecord(t0, cs), "event record");
+    if ((s = launch_pipe(device, dA, lda_d, dB, ldb_d, dC, ldc_d, Mq, k, n, st.dtab + 128, st.dtab, P, cs))) return s;
+    TB_CUDA(cudaEventRecord(t1, cs), "event record");
+    if ((s = d2h(cs, 0, Mq))) return s;
+  } else {
+    // Phase 1: panel p of every row group once it has landed; row group g
+    // stays on stream g, so its partial sums accumulate in panel order.
+    for (int p = 0; p < P; ++p)
+      for (int g = 0; g < G; ++g) {
+        TB_CUDA(cudaStreamWaitEvent(css[g], evP[p], 0), "stream wait");
+        if ((s = gemm(css[g], gb[g], gb[g + 1], pk[p], pk[p + 1], p > 0))) return s;
+        if (p == P - 1 && (s = d2h(css[g], gb[g], gb[g + 1]))) return s;
+      }
+  }
+  // Phase 2: full-K row blocks, alternating streams (the first one on the
+  // stream the fused phase-1 launch does not hold).
   for (int r = 0; r < R; ++r) {
-    const cudaStream_t cs = css[r & 1];
+    const cudaStream_t cs = css[(r + (fused ? 1 : 0)) & 1];
     TB_CUDA(cudaStreamWaitEvent(cs, evP[P - 1], 0), "stream wait");
     TB_CUDA(cudaStreamWaitEvent(cs, evA[r], 0), "stream wait");
     if ((s = gemm(cs, rb[r], rb[r + 1], 0, k, false))) return s;
@@ -1036,6 +1157,10 @@ void tb_release(void) {
       if (*sp) cudaStreamDestroy(*sp);
       *sp = nullptr;
     }
+    if (st.dtab) cudaFree(st.dtab);
+    if (st.htab) cudaFreeHost(st.htab);
+    st.dtab = nullptr;
+    st.htab = nullptr;
     for (auto& pool : st.ev_pool) {
       for (cudaEvent_t e : pool) cudaEventDestroy(e);
       pool.clear();

@@ -870,7 +870,8 @@ int tb_gpu_tiled_multiply_flat_ex(int32_t device, const double* a, const double*
     // Phase 1 as one persistent launch that waits on per-panel flags (PIPE
     // mode) rather than a launch per panel and row group; TB_PIPE_FUSED=0
     // restores the launch-per-panel form (A/B).
-    static const bool fused_env = !(std::getenv("TB_PIPE_FUSED") && std::strcmp(std::getenv("TB_PIPE_FUSED"), "0") == 0);
+    const char* fe = std::getenv("TB_PIPE_FUSED");
+    const bool fused_env = !(fe && std::strcmp(fe, "0") == 0);
     fused = fused_env && variant != TB_VARIANT_PAPER && variant != TB_VARIANT_DFMA &&
             variant != TB_VARIANT_DMMA_CPASYNC && cfg_smem(0) <= g_dev[device].smem_optin;
     if (fused && !std::getenv("TB_PIPE")) {

@@ -335,16 +335,19 @@ def test_accumulate_epilogue_many_tiles_per_cta(tb, variant):
     assert all(torch.equal(outs[0], o) for o in outs[1:])
 
 
+@pytest.mark.parametrize("fused", ["1", "0"])
 @pytest.mark.parametrize("shape", ["1024,128,640,384", "256,2,4000,4000", "100000,512,512,1"])
-def test_flat_pipeline_shapes(tb, oracle, monkeypatch, shape):
+def test_flat_pipeline_shapes(tb, oracle, monkeypatch, shape, fused):
     """Forced pipeline shapes (TB_PIPE=mq,kp0,kp,blk): many small panels and
-    blocks, a 2-wide first panel, all rows panelised — all equal the
+    blocks, a 2-wide first panel, all rows panelised — with phase 1 as the
+    fused flag-driven launch and as a launch per panel — all equal the
     single-launch result to the normwise bound."""
     import torch
 
     m, k, n = 4000, 3998, 4000
     a, b = oracle.generate(m, k, 3), oracle.generate(k, n, 4)
     monkeypatch.setenv("TB_PIPE", shape)
+    monkeypatch.setenv("TB_PIPE_FUSED", fused)
     c = np.zeros(m * n)
     out_s = np.zeros(1)
     assert tb.gpu_tiled_multiply_flat(0, a, b, m, k, n, 32, c, out_s) == tb.STATUS_OK

@@ -41,7 +41,7 @@ DEFAULT_TILE_EDGE = 32
 EXPORTS = [
     "tb_gpu_tiled_multiply_flat", "tb_gpu_tiled_multiply_flat_ex", "tb_dgemm", "tb_dgemm_launch",
     "tb_cublas_dgemm", "tb_validate_launch", "tb_device_count", "tb_variant_name",
-    "tb_resolve_variant", "tb_last_error", "tb_version", "tb_release",
+    "tb_resolve_variant", "tb_last_error", "tb_version", "tb_release", "tb_pipeline_plan",
 ]
 
 _D = ctypes.POINTER(ctypes.c_double)
@@ -78,8 +78,12 @@ def _declare(l):
     l.tb_version.restype = ctypes.c_char_p
     l.tb_release.argtypes = []
     l.tb_release.restype = None
+    _P64 = ctypes.POINTER(ctypes.c_int64)
+    _P32 = ctypes.POINTER(ctypes.c_int32)
+    l.tb_pipeline_plan.argtypes = [_I64, _I64, _I64, _I32, _I32, _P64, _P32, _P64, _I32, _P32, _P64, _I32, _P32]
     for name in ("tb_gpu_tiled_multiply_flat", "tb_gpu_tiled_multiply_flat_ex", "tb_dgemm", "tb_cublas_dgemm",
-                 "tb_dgemm_launch", "tb_validate_launch", "tb_device_count", "tb_resolve_variant"):
+                 "tb_dgemm_launch", "tb_validate_launch", "tb_device_count", "tb_resolve_variant",
+                 "tb_pipeline_plan"):
         getattr(l, name).restype = ctypes.c_int
 
 
@@ -121,6 +125,19 @@ def device_count() -> int:
 
 def version() -> str:
     return lib().tb_version().decode()
+
+
+def pipeline_plan(m: int, k: int, n: int, sms: int = 148, fused_ok: bool = True) -> dict:
+    """Shape of the host-buffer pipeline tb_gpu_tiled_multiply_flat_ex would
+    run for an m x k x n call (pure host computation; no device needed)."""
+    mq, fused = ctypes.c_int64(), ctypes.c_int32()
+    npan, nblk = ctypes.c_int32(), ctypes.c_int32()
+    panels = (ctypes.c_int64 * 256)()
+    blocks = (ctypes.c_int64 * 256)()
+    check(lib().tb_pipeline_plan(m, k, n, sms, 1 if fused_ok else 0, ctypes.byref(mq), ctypes.byref(fused), panels,
+                                 256, ctypes.byref(npan), blocks, 256, ctypes.byref(nblk)))
+    return {"mq": mq.value, "fused": bool(fused.value), "panels": list(panels[:npan.value]),
+            "blocks": list(blocks[:nblk.value])}
 
 
 def variant_id(variant) -> int:

@@ -1,0 +1,57 @@
+"""Host-buffer pipeline planner (tb_pipeline_plan, the shape
+tb_gpu_tiled_multiply_flat_ex runs) — pure host logic, no device needed."""
+import random
+
+import pytest
+
+from paper_2509_04594_b200 import _lib
+
+
+def _check(m, k, n, sms=148, fused_ok=True):
+    p = _lib.pipeline_plan(m, k, n, sms, fused_ok)
+    pan, blk, mq = p["panels"], p["blocks"], p["mq"]
+    assert pan[0] == 0 and pan[-1] == k and all(a < b for a, b in zip(pan, pan[1:]))
+    assert blk[0] == mq and blk[-1] == m and all(a < b for a, b in zip(blk, blk[1:]))
+    assert mq == m or (mq % 128 == 0 and 0 < mq < m)
+    align = 16 if p["fused"] else 2  # k-stage bounds for the fused PIPE launch, TMA (even k0) otherwise
+    assert all(x % align == 0 for x in pan[1:-1])
+    assert all(x % 128 == 0 for x in blk[1:-1])  # only the last row block may be ragged
+    if not fused_ok:
+        assert not p["fused"]
+    if 2.0 * m * n * k < 1e11:
+        assert (mq, pan, blk, p["fused"]) == (m, [0, k], [m], False)
+    if p["fused"]:
+        assert 2 <= len(pan) - 1 <= 120
+    return p
+
+
+def test_n10000_shape():
+    p = _check(10000, 10000, 10000)
+    # 34 tile rows cover the compute/transfer balance; 41 rows give 3239
+    # tiles = 21.89 per CTA on 148 SMs (least imbalance within +8 rows).
+    assert p["mq"] == 41 * 128 and p["fused"]
+    assert p["panels"][1] == 256  # small first panel: the GEMM starts after 0.56 ms of copies
+    assert p["blocks"][-1] - p["blocks"][-2] <= 512  # short final D2H
+
+
+def test_small_problems_are_single_shot():
+    for s in [(1, 1, 1), (1000, 1000, 1000), (3001, 2999, 2500), (100, 100000, 100)]:
+        _check(*s)
+
+
+def test_unfused_form():
+    p = _check(10000, 10000, 10000, fused_ok=False)
+    assert not p["fused"]
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_random_shapes(seed):
+    rng = random.Random(seed)
+    for _ in range(60):
+        m, k, n = (rng.randint(1, 40000) for _ in range(3))
+        _check(m, k, n, sms=rng.choice([148, 132, 8]), fused_ok=rng.random() < 0.8)
+
+
+def test_bad_arguments():
+    with pytest.raises(Exception):
+        _lib.pipeline_plan(0, 10, 10)

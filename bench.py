@@ -353,14 +353,15 @@ def run_ours(args) -> None:
             "check_vs_cublas_normwise": rel,
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "dgemm_dmma_kernel<6, TMA>", "flops_per_launch": flops_per_launch,
+                         "kernel": "dgemm_dmma_kernel<1, 6, TMA, DMMA, 128> (cross-stage prefetch)", "flops_per_launch": flops_per_launch,
                          "avg_launch_ms": avg_launch * 1e3, "peak_source": peak_src},
             "e2e": {"value": flop_count(n) / e2e_s / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3,
                     "device_event_value": flop_count(n) / e2e_dev_s / 1e9,
                     "path": "gpu_tiled_multiply_flat -> tb_gpu_tiled_multiply_flat_ex (the reference's flat FFI shape): "
-                            "pinned host A,B -> copy/compute pipeline (phase 1: K-panels of A[:Mq] and B with 2D copies; "
-                            "phase 2: full-K row blocks; C row blocks back as they finish) -> host C. value: host wall clock "
+                            "pinned host A,B -> copy/compute pipeline (phase 1: K-panels of A[:Mq] and B, 2D copies, consumed by "
+                            "one flag-driven persistent GEMM launch; phase 2: full-K row blocks; C row blocks back as they "
+                            "finish) -> host C. value: host wall clock "
                             "around the synchronous call (median); device_event_value: CUDA events first H2D -> last D2H"},
             "gpu_launches": args.steps * (1 if world == 1 else len(panel_bounds(n, args.panels))),
             "clocks": clk,

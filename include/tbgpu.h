@@ -76,7 +76,9 @@ TB_API int tb_gpu_tiled_multiply_flat(int32_t device, const double* a, const dou
 
 /* Same as above with an explicit variant and an optional end-to-end clock:
  * out_e2e_seconds (nullable) receives device time from the first H2D copy to
- * the end of the D2H copy, on one stream (the `e2e` bench leg). */
+ * the end of the last D2H copy (the `e2e` bench leg). Large calls run a
+ * copy/compute pipeline (shape: tb_pipeline_plan);
+ * out_seconds is then the sum of the GEMM launches' durations. */
 TB_API int tb_gpu_tiled_multiply_flat_ex(int32_t device, const double* a, const double* b,
                                   int64_t m, int64_t k, int64_t n, int32_t tile_edge,
                                   int32_t variant, double* out_c, int64_t out_c_len,

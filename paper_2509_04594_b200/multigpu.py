@@ -21,7 +21,7 @@ from typing import Callable
 import torch
 import torch.distributed as dist
 
-__all__ = ["row_partitions", "panel_bounds", "ShardedGemm", "gather_rows"]
+__all__ = ["row_partitions", "panel_bounds", "gathered_panels", "ShardedGemm", "HostShardedGemm", "gather_rows"]
 
 
 def row_partitions(m: int, world: int) -> list[tuple[int, int]]:
@@ -50,6 +50,25 @@ def panel_bounds(k: int, panels: int) -> list[tuple[int, int]]:
     out, k0 = [], 0
     while k0 < k:
         k1 = min(k, k0 + step)
+        out.append((k0, k1))
+        k0 = k1
+    return out
+
+
+def gathered_panels(k: int, world: int, panels: int) -> list[tuple[int, int]]:
+    """K-panels for the host-buffer path: every panel but the last spans a
+    multiple of 2*world rows of B, so each rank uploads an equal, even-sized
+    share and the panel is rebuilt by one equal-chunk all-gather; the last
+    panel's shares run past ``k`` (padding rows that are gathered but never
+    multiplied)."""
+    unit = 2 * world
+    kp = -(-k // unit) * unit                     # padded row count
+    panels = max(1, min(int(panels), kp // unit))
+    step = -(-kp // panels)
+    step = -(-step // unit) * unit
+    out, k0 = [], 0
+    while k0 < kp:
+        k1 = min(kp, k0 + step)
         out.append((k0, k1))
         k0 = k1
     return out
@@ -91,6 +110,107 @@ class ShardedGemm:
             if a_local.shape[0] > 0:
                 self.local_matmul(a_local[:, k0:k1], b[k0:k1], out_local, i > 0)
         return out_local
+
+
+class HostShardedGemm:
+    """End-to-end form over host buffers: ``C_local = A_local · B`` where each
+    rank holds its rows of A and C in (pinned) host memory and can read B's
+    rows from its own host copy.
+
+    B crosses PCIe once in total rather than once per GPU: for K-panel q each
+    rank uploads an equal share of the panel's rows over its own link, and one
+    NCCL all-gather over NVLink/NVSwitch rebuilds the panel on every rank; the
+    panel's GEMM ``C_local (+)= A_local[:, q] · B[q, :]`` runs as soon as its
+    gather completes. The last panel's GEMM is split into row chunks whose
+    D2H copies overlap the remaining chunks. Device buffers are cached across
+    calls. With ``device='cpu'`` (gloo tests) copies are plain copies."""
+
+    def __init__(self, group=None, panels: int = 4, chunks: int = 4, local_matmul: Callable | None = None,
+                 device=None):
+        self.group = group
+        self.panels = panels
+        self.chunks = chunks
+        self.local_matmul = local_matmul or _gpu_matmul
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self._bufs = None
+
+    def _buffers(self, m, k, kp, n, share_rows):
+        key = (m, k, kp, n, share_rows)
+        if self._bufs is None or self._bufs[0] != key:
+            dev = self.device
+            a = torch.empty((m, k), dtype=torch.float64, device=dev)
+            b = torch.empty((kp, n), dtype=torch.float64, device=dev)
+            c = torch.empty((m, n), dtype=torch.float64, device=dev)
+            stage = torch.zeros((share_rows, n), dtype=torch.float64, device=dev)  # this rank's shares; pad rows 0
+            self._bufs = (key, a, b, c, stage)
+        return self._bufs[1:]
+
+    def __call__(self, a_local_h: torch.Tensor, b_h: torch.Tensor, c_local_h: torch.Tensor) -> torch.Tensor:
+        world = dist.get_world_size(self.group)
+        rank = dist.get_rank(self.group)
+        m, k = a_local_h.shape
+        n = b_h.shape[1]
+        if b_h.shape[0] != k or tuple(c_local_h.shape) != (m, n):
+            raise ValueError(f"shapes {tuple(a_local_h.shape)} @ {tuple(b_h.shape)} -> {tuple(c_local_h.shape)}")
+        bounds = gathered_panels(k, world, self.panels)
+        kp = bounds[-1][1]
+        shares = [(k1 - k0) // world for k0, k1 in bounds]
+        a_d, b_d, c_d, stage = self._buffers(m, k, kp, n, sum(shares))
+        cuda = self.device.type == "cuda"
+        comp = torch.cuda.current_stream(self.device) if cuda else None
+        copy_s = torch.cuda.Stream(self.device) if cuda else None
+        back_s = torch.cuda.Stream(self.device) if cuda else None
+
+        def on(stream):
+            return torch.cuda.stream(stream) if stream is not None else _null()
+
+        # Uploads and gathers are issued from the copy stream, panel by panel:
+        # NCCL orders gather q after the uploads enqueued before it (this
+        # rank's shares of panels <= q, and A after panel 0's share).
+        works, off = [], 0
+        with on(copy_s):
+            if cuda:
+                copy_s.wait_stream(comp)  # the cached buffers are free once earlier compute is done
+            for q, (k0, k1) in enumerate(bounds):
+                sh = shares[q]
+                s0, s1 = k0 + rank * sh, min(k0 + (rank + 1) * sh, k)
+                if s1 > s0:
+                    stage[off:off + s1 - s0].copy_(b_h[s0:s1], non_blocking=cuda)
+                if q == 0:
+                    a_d.copy_(a_local_h, non_blocking=cuda)
+                works.append(dist.all_gather_into_tensor(b_d[k0:k1], stage[off:off + sh], group=self.group,
+                                                         async_op=True))
+                off += sh
+        step = -(-max(m, 1) // self.chunks)
+        step = -(-step // 128) * 128
+        for q, (k0, k1) in enumerate(bounds):
+            works[q].wait()  # the compute stream (not the host) waits for the gather
+            kk1 = min(k1, k)
+            if kk1 <= k0 or m == 0:
+                continue
+            if q < len(bounds) - 1:
+                self.local_matmul(a_d[:, k0:kk1], b_d[k0:kk1], c_d, q > 0)
+                continue
+            # last panel: row chunks, each copied back as soon as it is final
+            for r0 in range(0, m, step):
+                r1 = min(m, r0 + step)
+                self.local_matmul(a_d[r0:r1, k0:kk1], b_d[k0:kk1], c_d[r0:r1], q > 0)
+                if cuda:
+                    back_s.wait_stream(comp)
+                with on(back_s):
+                    c_local_h[r0:r1].copy_(c_d[r0:r1], non_blocking=cuda)
+        if cuda:
+            back_s.synchronize()  # synchronous call: C is in host memory on return
+            comp.wait_stream(back_s)
+        return c_local_h
+
+
+class _null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        return False
 
 
 def gather_rows(out_local: torch.Tensor, parts: list[tuple[int, int]], dst: int = 0, group=None):

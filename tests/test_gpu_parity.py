@@ -245,7 +245,7 @@ def test_sharded_gemm_single_rank_nccl_panels(tb, oracle):
     import torch
     import torch.distributed as dist
 
-    from paper_2509_04594_b200.multigpu import ShardedGemm, row_partitions
+    from paper_2509_04594_b200.multigpu import HostShardedGemm, ShardedGemm, row_partitions
 
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
     os.environ.setdefault("MASTER_PORT", "29533")
@@ -263,6 +263,15 @@ def test_sharded_gemm_single_rank_nccl_panels(tb, oracle):
             ShardedGemm(panels=panels)(ta, tb_, out)
             torch.cuda.synchronize()
             assert oracle.normwise_rel(out.cpu().numpy(), ref) <= NORMWISE
+        # end-to-end form from pinned host buffers (per-rank B shares + all-gather)
+        a_h = torch.from_numpy(a[r0:r1]).pin_memory()
+        b_h = torch.from_numpy(b).pin_memory()
+        for panels, chunks in ((1, 1), (4, 3), (7, 4)):
+            c_h = torch.full((r1 - r0, n), float("nan"), dtype=torch.float64).pin_memory()
+            g = HostShardedGemm(panels=panels, chunks=chunks)
+            for _ in range(2):
+                g(a_h, b_h, c_h)
+            assert oracle.normwise_rel(c_h.numpy(), ref) <= NORMWISE
     finally:
         dist.destroy_process_group()
 

@@ -11,7 +11,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2509_04594_b200.multigpu import ShardedGemm, gather_rows, panel_bounds, row_partitions
+from paper_2509_04594_b200.multigpu import (HostShardedGemm, ShardedGemm, gather_rows, gathered_panels, panel_bounds,
+                                            row_partitions)
 
 
 def _free_port():
@@ -83,3 +84,51 @@ def test_panel_bounds_even_and_covering():
             assert b[0][0] == 0 and b[-1][1] == k
             assert all(x[1] == y[0] for x, y in zip(b, b[1:]))
             assert all(k0 % 2 == 0 for k0, _ in b)
+
+
+def _host_worker(rank, world, port, m, k, n, panels, chunks, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        a = torch.from_numpy(np.random.Generator(np.random.PCG64(3)).random((m, k)) * 3 + 2)
+        b = torch.from_numpy(np.random.Generator(np.random.PCG64(4)).random((k, n)) * 3 + 2)
+        parts = row_partitions(m, world)
+        r0, r1 = parts[rank]
+        c = torch.full((r1 - r0, n), float("nan"), dtype=torch.float64)
+        g = HostShardedGemm(panels=panels, chunks=chunks, local_matmul=_cpu_matmul, device="cpu")
+        for _ in range(2):  # cached buffers reused by the second call
+            g(a[r0:r1].contiguous(), b, c)
+        full = gather_rows(c, parts, dst=0)
+        if rank == 0:
+            ref = (a @ b).numpy()
+            q.put(float(np.linalg.norm(full.numpy() - ref) / np.linalg.norm(ref)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("m,k,n,panels,chunks", [(37, 41, 29, 3, 2), (64, 64, 64, 1, 4), (5, 3, 7, 2, 1),
+                                                 (300, 200, 100, 4, 3)])
+def test_host_sharded_world2(m, k, n, panels, chunks):
+    """End-to-end multi-GPU form: B uploaded in equal per-rank shares per
+    K-panel and rebuilt by all-gather, last panel in row chunks copied back."""
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    port = _free_port()
+    procs = [ctx.Process(target=_host_worker, args=(r, 2, port, m, k, n, panels, chunks, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=120)
+    assert all(p.exitcode == 0 for p in procs)
+    assert q.get() <= 1e-12
+
+
+def test_gathered_panels_cover_and_divide():
+    for k in (1, 2, 3, 5, 37, 1000, 10000, 32768):
+        for world in (1, 2, 3, 4, 8):
+            for panels in (1, 2, 4, 7):
+                b = gathered_panels(k, world, panels)
+                assert b[0][0] == 0 and b[-1][1] >= k and b[-1][1] - k < 2 * world
+                assert all(x1 == y0 for (_, x1), (y0, _) in zip(b, b[1:]))
+                assert all((k1 - k0) % (2 * world) == 0 and k1 > k0 for k0, k1 in b)

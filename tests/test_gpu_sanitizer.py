@@ -37,20 +37,22 @@ def _sanitizer():
 
 
 def test_driver_plain(driver):
-    res = subprocess.run([driver], capture_output=True, text=True, timeout=300)
+    res = subprocess.run([driver, "--pipeline"], capture_output=True, text=True, timeout=300)
     assert res.returncode == 0, res.stdout + res.stderr
 
 
-@pytest.mark.parametrize("tool,args", [("memcheck", []), ("synccheck", []), ("racecheck", ["--tma-only"])])
-def test_sanitizer_clean(driver, tool, args):
+@pytest.mark.parametrize("bm", ["", "128"])
+@pytest.mark.parametrize("tool,args", [("memcheck", ["--pipeline"]), ("synccheck", []), ("racecheck", ["--tma-only"])])
+def test_sanitizer_clean(driver, tool, args, bm):
     """racecheck runs on the TMA-fed variants and the paper kernel only: it
     tracks 8-byte cp.async shared writes but not the mbarrier arrive/wait that
     orders them against the consumers' reads, so the cp.async loader (ordered
     by cp.async.wait_group + mbarrier release/acquire, dgemm_dmma.cuh) shows
     false hazards. Its correctness is covered by memcheck/synccheck here and by
     the bitwise-repeatability and parity tests."""
+    env = dict(os.environ, TB_BM=bm)  # "": choose_bm picks 64-row tiles for these shapes; "128" forces 128
     res = subprocess.run([_sanitizer(), "--tool", tool, "--error-exitcode", "3", driver, *args],
-                         capture_output=True, text=True, timeout=900)
+                         capture_output=True, text=True, timeout=900, env=env)
     out = res.stdout + res.stderr
     assert res.returncode == 0, out[-4000:]
     assert "ERROR SUMMARY: 0 errors" in out or "RACECHECK SUMMARY: 0 hazards" in out, out[-2000:]

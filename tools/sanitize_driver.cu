@@ -14,11 +14,18 @@
 
 #include "tbgpu.h"
 
-// Usage: sanitize_driver [--tma-only]
+// Usage: sanitize_driver [--tma-only] [--pipeline]
 //   --tma-only: even shapes and TMA-fed variants only (racecheck does not
 //   model mbarrier-ordered cp.async writes; see tests/test_gpu_sanitizer.py).
+//   --pipeline: also one host-buffer call large enough for the copy/compute
+//   pipeline (the flag-driven PIPE-mode phase-1 launch + row blocks).
+// TB_BM=128 in the environment forces the 128-row tiles on these small shapes.
 int main(int argc, char** argv) {
-  const bool tma_only = argc > 1 && std::string(argv[1]) == "--tma-only";
+  bool tma_only = false, pipeline = false;
+  for (int i = 1; i < argc; ++i) {
+    tma_only |= std::string(argv[i]) == "--tma-only";
+    pipeline |= std::string(argv[i]) == "--pipeline";
+  }
   struct Shape {
     long m, k, n;
   };
@@ -58,6 +65,28 @@ int main(int argc, char** argv) {
     cudaFree(dA);
     cudaFree(dB);
     cudaFree(dC);
+  }
+  if (pipeline) {
+    const long m = 2560, k = 8192, n = 2560;  // 1.07e11 flops: pipelined (phase 1 + row blocks)
+    std::vector<double> a(m * k), b(k * n), c(m * n);
+    for (size_t i = 0; i < a.size(); ++i) a[i] = 2.0 + 3.0 * ((i * 2654435761u) % 1000) / 1000.0;
+    for (size_t i = 0; i < b.size(); ++i) b[i] = 2.0 + 3.0 * ((i * 40503u) % 1000) / 1000.0;
+    double sec = 0, e2e = 0;
+    const int st = tb_gpu_tiled_multiply_flat_ex(0, a.data(), b.data(), m, k, n, 32, TB_VARIANT_AUTO, c.data(),
+                                                 (long)c.size(), &sec, &e2e);
+    // spot-check rows against a host dot product
+    double num = 0, den = 0;
+    for (long i = 0; i < m; i += 509)
+      for (long j = 0; j < n; j += 7) {
+        double r = 0;
+        for (long p = 0; p < k; ++p) r += a[i * k + p] * b[p * n + j];
+        num += (c[i * n + j] - r) * (c[i * n + j] - r);
+        den += r * r;
+      }
+    const double rel = std::sqrt(num / den);
+    const bool ok = st == TB_STATUS_OK && rel <= 1e-12;
+    failures += !ok;
+    std::printf("pipeline %ldx%ldx%ld status=%d normwise=%.2e %s\n", m, k, n, st, rel, ok ? "ok" : tb_last_error());
   }
   tb_release();
   return failures ? 1 : 0;

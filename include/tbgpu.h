@@ -140,6 +140,10 @@ TB_API int tb_pipeline_plan(int64_t m, int64_t k, int64_t n, int32_t sms, int32_
                             int32_t* out_fused, int64_t* out_panels, int32_t max_panels, int32_t* out_npanels,
                             int64_t* out_blocks, int32_t max_blocks, int32_t* out_nblocks);
 
+/* Number of kernels this library has launched so far in this process (its
+ * own GEMM, strip, pipeline and staging kernels; not cuBLAS). */
+TB_API long long tb_kernel_launches(void);
+
 /* Free the cached host-entry workspaces and cuBLAS handles. */
 TB_API void tb_release(void);
 

@@ -42,6 +42,7 @@ EXPORTS = [
     "tb_gpu_tiled_multiply_flat", "tb_gpu_tiled_multiply_flat_ex", "tb_dgemm", "tb_dgemm_launch",
     "tb_cublas_dgemm", "tb_validate_launch", "tb_device_count", "tb_variant_name",
     "tb_resolve_variant", "tb_last_error", "tb_version", "tb_release", "tb_pipeline_plan",
+    "tb_kernel_launches",
 ]
 
 _D = ctypes.POINTER(ctypes.c_double)
@@ -80,6 +81,8 @@ def _declare(l):
     l.tb_release.restype = None
     _P64 = ctypes.POINTER(ctypes.c_int64)
     _P32 = ctypes.POINTER(ctypes.c_int32)
+    l.tb_kernel_launches.argtypes = []
+    l.tb_kernel_launches.restype = ctypes.c_longlong
     l.tb_pipeline_plan.argtypes = [_I64, _I64, _I64, _I32, _I32, _P64, _P32, _P64, _I32, _P32, _P64, _I32, _P32]
     for name in ("tb_gpu_tiled_multiply_flat", "tb_gpu_tiled_multiply_flat_ex", "tb_dgemm", "tb_cublas_dgemm",
                  "tb_dgemm_launch", "tb_validate_launch", "tb_device_count", "tb_resolve_variant",
@@ -125,6 +128,11 @@ def device_count() -> int:
 
 def version() -> str:
     return lib().tb_version().decode()
+
+
+def kernel_launches() -> int:
+    """Kernels this library has launched in this process (tb_kernel_launches)."""
+    return int(lib().tb_kernel_launches())
 
 
 def pipeline_plan(m: int, k: int, n: int, sms: int = 148, fused_ok: bool = True) -> dict:

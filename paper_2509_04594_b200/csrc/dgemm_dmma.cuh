@@ -44,10 +44,10 @@ enum class Math : int { DMMA = 0, DFMA = 1 };
 // BM (tile rows) is a template parameter: 128 is the production tile; 64
 // halves the row padding and doubles the tile count for small problems
 // (warp tile 32 x 32). Everything else is shared.
-template <int BM_>
+template <int BM_, int BN_ = 128, int WARPS_M_ = 2>
 struct DmmaCfgT {
-  static constexpr int BM = BM_, BN = 128, BK = 16;
-  static constexpr int WARPS_M = 2, WARPS_N = 4;
+  static constexpr int BM = BM_, BN = BN_, BK = 16;
+  static constexpr int WARPS_M = WARPS_M_, WARPS_N = 8 / WARPS_M_;
   static constexpr int WM = BM / WARPS_M;  // 64
   static constexpr int WN = BN / WARPS_N;  // 32
   static constexpr int MI = WM / 8;        // 8 DMMA rows per warp
@@ -71,9 +71,9 @@ struct DmmaCfgT {
 using DmmaCfg = DmmaCfgT<128>;
 
 // A pipeline stage holds SUB consecutive 16-deep k sub-slabs (SUB * STAGE bytes).
-template <int SUB, int STAGES, int BM = 128>
+template <int SUB, int STAGES, int BM = 128, int BN = 128>
 constexpr int dmma_smem_bytes() {
-  return STAGES * SUB * DmmaCfgT<BM>::STAGE + 2 * STAGES * 8 + 16 + 1024;  // + barriers + flag + alignment slack
+  return STAGES * SUB * DmmaCfgT<BM, BN>::STAGE + 2 * STAGES * 8 + 16 + 1024;  // + barriers + flag + alignment slack
 }
 
 struct GemmParams {
@@ -183,11 +183,14 @@ struct PipeIter {
 
 __device__ __forceinline__ void consumer_bar() { asm volatile("bar.sync 1, %0;\n" ::"n"(DmmaCfg::CONSUMER_THREADS)); }
 
-template <int SUB, int STAGES, Loader LD, Math MT = Math::DMMA, int BM = 128, bool PIPE = false>
+template <int SUB, int STAGES, Loader LD, Math MT = Math::DMMA, int BM = 128, bool PIPE = false, int BN = 128,
+          int WARPS_M = 2>
 __global__ void __launch_bounds__(DmmaCfg::THREADS, 1)
     dgemm_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       const GemmParams p) {
-  using C = DmmaCfgT<BM>;
+  using C = DmmaCfgT<BM, BN, WARPS_M>;
+  static_assert(C::WARPS_M * C::WARPS_N == 8 && C::MI >= 2 && C::WN % 16 == 0, "8 consumer warps, >= 16 x 16 each");
+  static_assert(MT == Math::DMMA || (BN == 128 && WARPS_M == 2), "the DFMA comparison path is laid out for 128 x 128");
   using Iter = typename std::conditional<PIPE, PipeIter, WorkIter>::type;
   static_assert(!PIPE || (LD == Loader::TMA && MT == Math::DMMA), "PIPE mode: TMA + DMMA only");
   static_assert(MT == Math::DMMA || BM == 128, "the DFMA comparison path is laid out for 128-row tiles");
@@ -285,7 +288,7 @@ __global__ void __launch_bounds__(DmmaCfg::THREADS, 1)
             }
 #pragma unroll 4
             for (int i = 0; i < (C::BK * C::BN) / 128; ++i) {
-              const int e = i * 128 + pt, kr = e >> 7, nn = e & 127;
+              const int e = i * 128 + pt, kr = e / C::BN, nn = e % C::BN;
               const int gk = k0 + kr, gn = n0 + nn;
               const bool ok = gk < p.k && gn < p.n;
               const double* src = ok ? p.B + (int64_t)gk * p.ldb + gn : p.B;
@@ -352,7 +355,7 @@ __global__ void __launch_bounds__(DmmaCfg::THREADS, 1)
     const int kv[4] = {2 * pa, 2 * pa + 1, 2 * pb, 2 * pb + 1};
 #pragma unroll
     for (int e = 0; e < 4; ++e)
-      b_off[e] = wn * 2 * C::B_BOX + kv[e] * 128 + ((((g >> 1) ^ (kv[e] & 7))) << 4) + (g & 1) * 8;
+      b_off[e] = wn * (C::WN / 16) * C::B_BOX + kv[e] * 128 + ((((g >> 1) ^ (kv[e] & 7))) << 4) + (g & 1) * 8;
   }
 
   int s = 0;

@@ -276,7 +276,8 @@ def test_sharded_gemm_single_rank_nccl_panels(tb, oracle):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("m,k,n", [(4000, 4000, 4000), (3001, 2999, 2500), (7000, 4999, 6000)])
+@pytest.mark.parametrize("m,k,n", [(4000, 4000, 4000), (3001, 2999, 2500), (7000, 4999, 6000), (7000, 4000, 6032),
+                                   (5100, 3000, 9999)])
 def test_flat_pipelined_host_path(tb, golden, oracle, m, k, n):
     """Large host-buffer calls run the copy/compute pipeline (phase 1: K-panels
     of the first Mq rows with 2D copies of A's panel slices; phase 2: full-K
@@ -363,6 +364,26 @@ def test_flat_pipeline_shapes(tb, oracle, monkeypatch, shape, fused):
     ref, _ = tb.cublas_dgemm(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda())
     got = torch.from_numpy(c.reshape(m, n)).cuda()
     assert (torch.linalg.norm(got - ref) / torch.linalg.norm(ref)).item() <= NORMWISE
+
+
+@pytest.mark.parametrize("m,k,n", [(2320, 600, 2320), (2336, 500, 2368), (2368, 300, 2340), (4001, 257, 3999)])
+def test_edge_strip_split(tb, oracle, m, k, n):
+    """Large TMA products with ragged m / n run as a whole-tile launch plus
+    edge strips (16/32/64-row and 32/64-column strip shapes); C, plain and
+    accumulated, equals the oracle's rows and cuBLAS normwise."""
+    import torch
+
+    a, b = oracle.generate(m, k, 41), oracle.generate(k, n, 42)
+    ta, tbm = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    c, sec = tb.dgemm(ta, tbm)
+    rows = np.r_[0:3, m - 70:m]  # first rows and the bottom strip
+    assert oracle.normwise_rel(c.cpu().numpy()[rows], oracle.tiled_parallel(a[rows], b)) <= NORMWISE
+    ref, _ = tb.cublas_dgemm(ta, tbm)
+    assert (torch.linalg.norm(c - ref) / torch.linalg.norm(ref)).item() <= NORMWISE
+    out = ref.clone()
+    tb.dgemm_launch(ta, tbm, out, accumulate=True)
+    torch.cuda.synchronize()
+    assert (torch.linalg.norm(out - 2 * ref) / torch.linalg.norm(2 * ref)).item() <= NORMWISE
 
 
 def test_staged_tma_for_misaligned_operands(tb, oracle):

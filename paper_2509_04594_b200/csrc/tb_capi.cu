@@ -90,7 +90,15 @@ void* pipe_kernel() { return (void*)tb::dgemm_dmma_kernel<1, 6, tb::Loader::TMA,
 // large product, so the main launch runs on whole 128 x 128 tiles and only a
 // narrow strip pads (N = 10000: the last tile column and row had 16 valid
 // columns / rows of 128, 2.2 % of all DMMAs on zeros).
-enum StripCfg : int { kStripNone = 0, kStrip128x32, kStrip128x64, kStrip16x128, kStrip32x128, kStrip64x128 };
+enum StripCfg : int {
+  kStripNone = 0,
+  kStrip128x16,
+  kStrip128x32,
+  kStrip128x64,
+  kStrip16x128,
+  kStrip32x128,
+  kStrip64x128
+};
 constexpr int kStripStages = 8;
 template <int BM, int BN, int WM>
 struct StripK {
@@ -106,6 +114,7 @@ struct StripInfo {
 };
 StripInfo strip_info(int c) {
   switch (c) {
+    case kStrip128x16: return {128, 16, StripK<128, 16, 8>::fn(), StripK<128, 16, 8>::smem()};
     case kStrip128x32: return {128, 32, StripK<128, 32, 8>::fn(), StripK<128, 32, 8>::smem()};
     case kStrip128x64: return {128, 64, StripK<128, 64, 4>::fn(), StripK<128, 64, 4>::smem()};
     case kStrip16x128: return {16, 128, StripK<16, 128, 1>::fn(), StripK<16, 128, 1>::smem()};
@@ -248,7 +257,7 @@ int ensure_kernel_attrs(int dev) {
   if (cfg_smem(0) <= st.smem_optin)
     TB_CUDA(cudaFuncSetAttribute(pipe_kernel(), cudaFuncAttributeMaxDynamicSharedMemorySize, cfg_smem(0)),
             "set smem attribute (pipe)");
-  for (int c = kStrip128x32; c <= kStrip32x128; ++c) {
+  for (int c = kStrip128x16; c <= kStrip32x128; ++c) {
     const StripInfo si = strip_info(c);
     if (si.smem <= st.smem_optin)
       TB_CUDA(cudaFuncSetAttribute(si.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, si.smem),
@@ -567,7 +576,8 @@ int launch(int dev, const double* A, int64_t lda, const double* B, int64_t ldb, 
     const int64_t hb = m % 128, wr = n % 128;
     const int bcfg = hb == 0 ? kStripNone : hb <= 16 ? kStrip16x128 : hb <= 32 ? kStrip32x128
                                                       : hb <= 64 ? kStrip64x128 : kStripNone;
-    const int rcfg = wr == 0 ? kStripNone : wr <= 32 ? kStrip128x32 : wr <= 64 ? kStrip128x64 : kStripNone;
+    const int rcfg = wr == 0 ? kStripNone : wr <= 16 ? kStrip128x16 : wr <= 32 ? kStrip128x32
+                                                      : wr <= 64 ? kStrip128x64 : kStripNone;
     const int64_t m1 = bcfg != kStripNone ? m - hb : m, n1 = rcfg != kStripNone ? n - wr : n;
     if ((bcfg != kStripNone || rcfg != kStripNone) && m1 >= 128 && n1 >= 128 &&
         choose_bm(m1, n1, g_dev[dev].sms, false) == 128) {
@@ -1230,7 +1240,7 @@ int tb_gpu_tiled_multiply_flat_ex(int32_t device, const double* a, const double*
     kt1.push_back(t1);
     TB_CUDA(cudaEventRecord(t0, cs), "event record");
     int rc = launch_tiles(device, dA, lda_d, dB + n1, ldb_d, dC + n1, ldc_d, m, k, wr, 0, tile_edge,
-                          TB_VARIANT_DMMA_TMA, cs, wr <= 32 ? kStrip128x32 : kStrip128x64);
+                          TB_VARIANT_DMMA_TMA, cs, wr <= 16 ? kStrip128x16 : wr <= 32 ? kStrip128x32 : kStrip128x64);
     if (rc) return rc;
     TB_CUDA(cudaEventRecord(t1, cs), "event record");
     return d2h(cs, 0, m, n1, n);

@@ -916,7 +916,7 @@ PipePlan plan_pipeline(int64_t m, int64_t k, int64_t n, int sms, bool fused_ok) 
                                      : std::vector<int64_t>{0, Mq};
     int64_t r = m - Mq;
     std::vector<int64_t> tail;
-    for (int64_t t : {std::min<int64_t>(256, blk / 4), blk / 2})  // shrinking tail: the last D2H is <= 20 MB
+    for (int64_t t : {std::min<int64_t>(128, blk / 4), blk / 2})  // shrinking tail: the last D2H is ~10-20 MB
       if (t > 0 && r >= 2 * t) {
         tail.push_back(t);
         r -= t;

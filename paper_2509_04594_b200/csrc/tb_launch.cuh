@@ -1,0 +1,461 @@
+// tb_launch.cuh — enqueueing GEMMs (included by tb_capi.cu only): the
+// persistent schedule shapes, stream-K / staging workspaces, the re-pitch
+// staging kernel, launch() with its edge-strip split, launch_tiles(), the
+// host pipeline's PIPE-mode launch and the event-timed synchronous call.
+#pragma once
+
+namespace {
+
+// Persistent schedule (dgemm_dmma.cuh): data-parallel tiles round-robin over
+// the CTAs, then a stream-K region whose k-iterations are split evenly across
+// them. Three shapes, chosen on the host (the kernel is the same):
+//  - stream-K: the last (T mod P) + P tiles split over P = #SM CTAs;
+//  - data-parallel: no split when a single wave is >= 75 % full — splitting
+//    every tile costs partial-tile traffic and fixups that an idle 10 % does
+//    not (measured: with several waves the stream-K tail still wins);
+//  - split-K: T <= P/2 tiles each split into exactly s = P / T equal k-ranges
+//    on s*T CTAs (num_k padded up to a multiple of s with k-slabs past K,
+//    which the loaders zero-fill), so every CTA owns exactly one segment and
+//    every tile exactly s — the stream-K split of so few tiles would give
+//    3-4 segments per tile and two fixups to some CTAs.
+// TB_SCHED=dp|sk forces data-parallel / the plain stream-K shape (A/B experiments).
+struct Schedule {
+  int grid, dp, sk, ipc, max_seg, num_k;
+};
+
+Schedule plan_schedule(int64_t tiles, int num_k, int sms) {
+  static const int forced = [] {
+    const char* e = std::getenv("TB_SCHED");
+    if (e && std::strcmp(e, "dp") == 0) return 1;
+    if (e && std::strcmp(e, "sk") == 0) return 2;  // always the stream-K shape (previous default)
+    return 0;
+  }();
+  Schedule sc{sms, (int)tiles, 0, 1, 1, num_k};
+  const int64_t rem = tiles % sms;
+  if (forced == 1 || rem == 0) return sc;
+  // A single wave >= 75 % full runs data-parallel: splitting every tile of a single wave costs about a
+  // quarter of a tile's k-loop in partial traffic and fixups (N = 1500, 144 tiles: 28.6 -> 31.2;
+  // N = 1000 on 64-row tiles, 128 tiles: 23.3 -> 25.9; N = 900, 120 tiles: 19.5 -> 20.5; at 61 %,
+  // N = 800, stream-K stays ahead 18.2 vs 15.9 TFLOP/s). With more waves the stream-K tail wins
+  // (N = 4000 / 6000 at 92 %: 34.12 / 35.84 vs 33.99 / 35.76).
+  if (forced == 0 && tiles < sms && 4 * tiles >= 3 * sms) return sc;
+  const int64_t min_seg = num_k < 8 ? num_k : 8;      // keep segments long enough to amortise the fixup
+  if (forced == 0 && 2 * tiles <= sms) {
+    int64_t split = std::min<int64_t>(sms / tiles, num_k / min_seg);
+    if (split >= 2) {
+      const int64_t ipc = (num_k + split - 1) / split;
+      sc.num_k = (int)(ipc * split);
+      sc.grid = (int)(split * tiles);
+      sc.dp = 0;
+      sc.sk = (int)tiles;
+      sc.ipc = (int)ipc;
+      sc.max_seg = (int)split;
+      return sc;
+    }
+  }
+  sc.sk = (int)(tiles > sms ? rem + sms : tiles);
+  sc.dp = (int)(tiles - sc.sk);
+  const int64_t total = (int64_t)sc.sk * num_k;
+  int64_t ipc = (total + sms - 1) / sms;
+  if (ipc < min_seg) ipc = min_seg;
+  sc.ipc = (int)ipc;
+  int max_seg = 1;
+  for (int64_t st = 0; st < sc.sk; ++st) {
+    const int64_t first = st * num_k;
+    const int64_t nseg = (first + num_k - 1) / ipc - first / ipc + 1;
+    if (nseg > max_seg) max_seg = (int)nseg;
+  }
+  sc.max_seg = max_seg;
+  return sc;
+}
+
+int split_workspace(int dev, cudaStream_t stream, size_t partial_elems, size_t counter_elems, double** partials,
+                    int** counters) {
+  DeviceState& st = g_dev[dev];
+  std::lock_guard<std::mutex> lk(st.mu);
+  DeviceState::SplitWs& w = st.split_ws[stream];
+  // Size for the schedule's bound on first use (plan_schedule: at most
+  // 2P - 1 stream-K tiles of at most 2 segments when T > P, at most P + T
+  // slots when T <= P), so a stream never regrows while its earlier launches
+  // may still be queued.
+  partial_elems = std::max(partial_elems, (size_t)4 * st.sms * tb::DmmaCfg::TILE_ELEMS);
+  counter_elems = std::max(counter_elems, (size_t)2 * st.sms);
+  if ((w.partial_elems < partial_elems && w.partials) || (w.counter_elems < counter_elems && w.counters))
+    TB_CUDA(cudaStreamSynchronize(stream), "stream-K workspace regrow");  // earlier launches may use it
+  if (w.partial_elems < partial_elems) {
+    if (w.partials) cudaFree(w.partials);
+    w.partials = nullptr;
+    w.partial_elems = 0;
+    TB_CUDA(cudaMalloc(&w.partials, partial_elems * sizeof(double)), "stream-K workspace allocation");
+    w.partial_elems = partial_elems;
+  }
+  if (w.counter_elems < counter_elems) {
+    if (w.counters) cudaFree(w.counters);
+    w.counters = nullptr;
+    w.counter_elems = 0;
+    TB_CUDA(cudaMalloc(&w.counters, counter_elems * sizeof(int)), "stream-K counter allocation");
+    // Counters start at zero once; each launch's last segment resets its tile's
+    // counter. Zeroed on the launching stream: a legacy-stream memset is not
+    // ordered before kernels on non-blocking streams.
+    TB_CUDA(cudaMemsetAsync(w.counters, 0, counter_elems * sizeof(int), stream), "stream-K counter init");
+    w.counter_elems = counter_elems;
+  }
+  *partials = w.partials;
+  *counters = w.counters;
+  return TB_STATUS_OK;
+}
+
+// Enqueue one GEMM on `stream` (current device = dev). Assumes validated args.
+// AUTO on operands TMA cannot address (odd leading dimension or a base not
+// 16-byte aligned — the reference's odd-N cases) would run the cp.async
+// loader at ~92 % of the TMA path's speed. For large products the operands
+// are instead copied once, on the launching stream, into even-pitch
+// workspace buffers (HBM copy: ~1 % of the GEMM time at N = 9999) and the
+// TMA kernel runs on those. Small products keep the cp.async loader.
+constexpr double kStageMinFlops = 2e10;
+constexpr size_t kStageMaxBytes = size_t(16) << 30;
+
+// Row re-pitch for staging: dst (16-byte aligned, even pitch) <- src (any
+// 8-byte alignment/pitch). One block row-slab per blockIdx.y, coalesced 8-byte
+// loads, 16-byte stores where the destination allows.
+__global__ void __launch_bounds__(256) repitch_kernel(const double* __restrict__ src, int64_t lds,
+                                                      double* __restrict__ dst, int64_t ldd, int64_t rows,
+                                                      int64_t cols) {
+  for (int64_t r = blockIdx.y; r < rows; r += gridDim.y) {
+    const double* s = src + r * lds;
+    double2* d = reinterpret_cast<double2*>(dst + r * ldd);
+    for (int64_t c = 2 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x); c < cols;
+         c += 2 * (int64_t)gridDim.x * blockDim.x) {
+      const double x = s[c];
+      const double y = c + 1 < cols ? s[c + 1] : 0.0;
+      d[c >> 1] = make_double2(x, y);  // ldd even and >= cols + (cols & 1): the pad column takes 0
+    }
+  }
+}
+
+int repitch(const double* src, int64_t lds, double* dst, int64_t ldd, int64_t rows, int64_t cols,
+            cudaStream_t stream) {
+  const int64_t pairs = (cols + 1) / 2;
+  const unsigned gx = (unsigned)std::min<int64_t>((pairs + 255) / 256, 8);
+  const unsigned gy = (unsigned)std::min<int64_t>(rows, 65535);
+  repitch_kernel<<<dim3(gx, gy), 256, 0, stream>>>(src, lds, dst, ldd, rows, cols);
+  TB_CUDA(cudaGetLastError(), "staging copy launch");
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return TB_STATUS_OK;
+}
+
+bool misaligned(const void* p, int64_t ld) { return (reinterpret_cast<uintptr_t>(p) & 15u) != 0 || (ld % 2) != 0; }
+
+int stage_workspace(int dev, cudaStream_t stream, size_t elems, double** buf) {
+  DeviceState& st = g_dev[dev];
+  std::lock_guard<std::mutex> lk(st.mu);
+  DeviceState::StageWs& w = st.stage_ws[stream];
+  if (w.elems < elems) {
+    if (w.buf) {
+      TB_CUDA(cudaStreamSynchronize(stream), "staging workspace regrow");  // earlier launches may use it
+      cudaFree(w.buf);
+    }
+    w.buf = nullptr;
+    w.elems = 0;
+    TB_CUDA(cudaMalloc(&w.buf, elems * sizeof(double)), "staging workspace allocation");
+    w.elems = elems;
+  }
+  *buf = w.buf;
+  return TB_STATUS_OK;
+}
+
+int launch_tiles(int dev, const double* A, int64_t lda, const double* B, int64_t ldb, double* Cm, int64_t ldc,
+                 int64_t m, int64_t k, int64_t n, int accumulate, int tile_edge, int variant, cudaStream_t stream,
+                 int strip);
+
+// Enqueue one GEMM on `stream` (current device = dev). Assumes validated args.
+// Stages misaligned operands (large AUTO calls), then, for a large TMA-fed
+// DMMA product whose m or n is not a multiple of 128, runs the whole-tile
+// part and the remainder strips as separate launches (TB_SPLIT=0: one
+// launch, A/B).
+int launch(int dev, const double* A, int64_t lda, const double* B, int64_t ldb, double* Cm, int64_t ldc, int64_t m,
+           int64_t k, int64_t n, int accumulate, int tile_edge, int variant, cudaStream_t stream) {
+  int s = ensure_kernel_attrs(dev);
+  if (s) return s;
+  if (variant == TB_VARIANT_AUTO && !tma_ok(A, lda, B, ldb) && 2.0 * (double)m * (double)n * (double)k >= kStageMinFlops) {
+    const bool sa = misaligned(A, lda), sb = misaligned(B, ldb);
+    const int64_t lda2 = (k + 1) & ~int64_t(1), ldb2 = (n + 1) & ~int64_t(1);
+    const size_t ea = sa ? (size_t)(m * lda2 + 32) : 0, eb = sb ? (size_t)(k * ldb2) : 0;
+    if ((ea + eb) * sizeof(double) <= kStageMaxBytes) {
+      double* buf = nullptr;
+      if ((s = stage_workspace(dev, stream, ea + eb + 32, &buf))) return s;
+      double* a2 = buf;
+      double* b2 = buf + ((ea + 31) & ~size_t(31));  // 256-byte aligned
+      if (sa) {
+        if ((s = repitch(A, lda, a2, lda2, m, k, stream))) return s;
+        A = a2;
+        lda = lda2;
+      }
+      if (sb) {
+        if ((s = repitch(B, ldb, b2, ldb2, k, n, stream))) return s;
+        B = b2;
+        ldb = ldb2;
+      }
+    }
+  }
+  variant = resolve(A, lda, B, ldb, variant);
+  static const bool split_env = !(std::getenv("TB_SPLIT") && std::strcmp(std::getenv("TB_SPLIT"), "0") == 0);
+  if (split_env && variant == TB_VARIANT_DMMA_TMA && (m % 128 != 0 || n % 128 != 0)) {
+    const int64_t hb = m % 128, wr = n % 128;
+    const int bcfg = hb == 0 ? kStripNone : hb <= 16 ? kStrip16x128 : hb <= 32 ? kStrip32x128
+                                                      : hb <= 64 ? kStrip64x128 : kStripNone;
+    const int rcfg = wr == 0 ? kStripNone : wr <= 16 ? kStrip128x16 : wr <= 32 ? kStrip128x32
+                                                      : wr <= 64 ? kStrip128x64 : kStripNone;
+    const int64_t m1 = bcfg != kStripNone ? m - hb : m, n1 = rcfg != kStripNone ? n - wr : n;
+    if ((bcfg != kStripNone || rcfg != kStripNone) && m1 >= 128 && n1 >= 128 &&
+        choose_bm(m1, n1, g_dev[dev].sms, false) == 128) {
+      // Main part on whole 128 x 128 tiles, then the right strip (all rows)
+      // and the bottom strip (the main part's columns); disjoint parts of C.
+      if ((s = launch_tiles(dev, A, lda, B, ldb, Cm, ldc, m1, k, n1, accumulate, tile_edge, variant, stream, -1)))
+        return s;
+      if (rcfg != kStripNone &&
+          (s = launch_tiles(dev, A, lda, B + n1, ldb, Cm + n1, ldc, m, k, n - n1, accumulate, tile_edge, variant,
+                            stream, rcfg)))
+        return s;
+      if (bcfg != kStripNone &&
+          (s = launch_tiles(dev, A + m1 * lda, lda, B, ldb, Cm + m1 * ldc, ldc, m - m1, k, n1, accumulate,
+                            tile_edge, variant, stream, bcfg)))
+        return s;
+      return TB_STATUS_OK;
+    }
+  }
+  return launch_tiles(dev, A, lda, B, ldb, Cm, ldc, m, k, n, accumulate, tile_edge, variant, stream, kStripNone);
+}
+
+// One launch on resolved operands. strip: kStripNone = choose_bm's tile
+// height, -1 = 128 x 128 forced, else an edge-strip shape.
+int launch_tiles(int dev, const double* A, int64_t lda, const double* B, int64_t ldb, double* Cm, int64_t ldc,
+                 int64_t m, int64_t k, int64_t n, int accumulate, int tile_edge, int variant, cudaStream_t stream,
+                 int strip) {
+  int s = TB_STATUS_OK;
+  if (variant == TB_VARIANT_PAPER) {
+    const int K = tile_edge;
+    dim3 block(K, K);
+    dim3 grid((unsigned)((n + K - 1) / K), (unsigned)((m + K - 1) / K));
+    tb::dgemm_paper_kernel<<<grid, block, 2 * K * K * sizeof(double), stream>>>(
+        A, lda, B, ldb, Cm, ldc, (int)m, (int)k, (int)n, K, accumulate);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+  } else {
+    using Cfg = tb::DmmaCfg;
+    tb::GemmParams p;
+    p.A = A;
+    p.B = B;
+    p.C = Cm;
+    p.lda = lda;
+    p.ldb = ldb;
+    p.ldc = ldc;
+    p.m = (int)m;
+    p.n = (int)n;
+    p.k = (int)k;
+    const bool dfma = variant == TB_VARIANT_DFMA;
+    const StripInfo si = strip > 0 ? strip_info(strip) : StripInfo{0, 0, nullptr, 0};
+    const bool narrow = si.fn != nullptr;  // an edge-strip shape (TMA only)
+    const int bm = narrow ? si.bm : strip == kStrip64x128 ? 64 : strip < 0 ? 128 : choose_bm(m, n, g_dev[dev].sms, dfma);
+    const int bn = narrow ? si.bn : Cfg::BN;
+    p.tiles_m = (int)((m + bm - 1) / bm);
+    p.tiles_n = (int)((n + bn - 1) / bn);
+    p.accumulate = accumulate;
+    p.vec_store = ((reinterpret_cast<uintptr_t>(Cm) & 15u) == 0 && ldc % 2 == 0) ? 1 : 0;
+    const int64_t tiles = (int64_t)p.tiles_m * p.tiles_n;
+    if (tiles > 0x7fffffff) {
+      set_err("too many output tiles");
+      return TB_STATUS_OVER_LIMITS;
+    }
+    const int cfg = dfma ? 0 : active_cfg();
+    const int64_t kstage = (bm == 64 || narrow) ? (int64_t)Cfg::BK : (int64_t)Cfg::BK * kCfgs[cfg].sub;
+    p.num_k = (int)((k + kstage - 1) / kstage);
+    const Schedule sc = plan_schedule(tiles, p.num_k, g_dev[dev].sms);
+    p.num_k = sc.num_k;  // split-K pads the k-slab count (extra slabs read as zeros)
+    p.dp_tiles = sc.dp;
+    p.sk_tiles = sc.sk;
+    p.sk_ipc = sc.ipc;
+    p.max_seg = sc.max_seg;
+    p.partials = nullptr;
+    p.counters = nullptr;
+#ifdef TB_TIMELINE
+    unsigned long long* tl_buf = nullptr;
+    p.timeline = nullptr;
+    if (std::getenv("TB_TIMELINE")) {
+      TB_CUDA(cudaMalloc(&tl_buf, (size_t)sc.grid * 8 * sizeof(unsigned long long)), "timeline alloc");
+      TB_CUDA(cudaMemsetAsync(tl_buf, 0, (size_t)sc.grid * 8 * sizeof(unsigned long long), stream), "timeline");
+      p.timeline = tl_buf;
+    }
+#endif
+    if (sc.sk > 0 &&
+        (s = split_workspace(dev, stream, (size_t)sc.sk * sc.max_seg * Cfg::TILE_ELEMS, (size_t)sc.sk, &p.partials,
+                             &p.counters)))
+      return s;
+    CUtensorMap mA, mB;
+    std::memset(&mA, 0, sizeof(mA));
+    std::memset(&mB, 0, sizeof(mB));
+    const bool use_tma = variant == TB_VARIANT_DMMA_TMA || (dfma && tma_ok(A, lda, B, ldb));
+    if (use_tma) {
+      if ((s = get_encoder())) return s;
+      if ((s = encode_map(&mA, A, m, k, lda, (uint32_t)bm))) return s;
+      if ((s = encode_map(&mB, B, k, n, ldb, Cfg::BK))) return s;
+    }
+    void* args[] = {&mA, &mB, &p};
+    if (narrow && !use_tma) {
+      set_err("edge-strip launch needs TMA-addressable operands");
+      return TB_STATUS_RUNTIME;
+    }
+    TB_CUDA(cudaLaunchKernel(narrow ? si.fn : bm == 64 ? small_kernel(use_tma) : cfg_kernel(cfg, use_tma, dfma),
+                             dim3((unsigned)sc.grid), dim3(Cfg::THREADS), args,
+                             (size_t)(narrow ? si.smem : bm == 64 ? small_smem() : cfg_smem(cfg)), stream),
+            "kernel launch");
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+#ifdef TB_TIMELINE
+    if (tl_buf) {
+      // Per-CTA stamps (ns): [0] entry [1] first stage landed [2] last main-loop end [3] last unit done
+      // [4] units [5] fixup ns [6] epilogue ns [7] main-loop ns.
+      std::vector<unsigned long long> h((size_t)sc.grid * 8);
+      TB_CUDA(cudaStreamSynchronize(stream), "timeline sync");
+      TB_CUDA(cudaMemcpy(h.data(), tl_buf, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost), "tl");
+      cudaFree(tl_buf);
+      unsigned long long t0 = ~0ull, tend = 0;
+      double first = 0, mainl = 0, fix = 0, epi = 0, units = 0, endmax = 0, endmin = 1e30, lastml = 0;
+      for (int c = 0; c < sc.grid; ++c) {
+        const unsigned long long* r = &h[(size_t)c * 8];
+        t0 = std::min(t0, r[0]);
+        tend = std::max(tend, r[3]);
+      }
+      for (int c = 0; c < sc.grid; ++c) {
+        const unsigned long long* r = &h[(size_t)c * 8];
+        first += (double)(r[1] - t0);
+        lastml += (double)(r[2] - t0);
+        mainl += (double)r[7];
+        fix += (double)r[5];
+        epi += (double)r[6];
+        units += (double)r[4];
+        endmax = std::max(endmax, (double)(r[3] - t0));
+        endmin = std::min(endmin, (double)(r[3] - t0));
+      }
+      const double g = sc.grid;
+      std::fprintf(stderr,
+                   "TBTIMELINE m=%lld n=%lld k=%lld grid=%d dp=%d sk=%d ipc=%d maxseg=%d span_us=%.2f "
+                   "first_stage_us=%.2f mainloop_us=%.2f last_mainloop_end_us=%.2f fixup_us=%.2f epilogue_us=%.2f "
+                   "units=%.2f end_min_us=%.2f end_max_us=%.2f\n",
+                   (long long)m, (long long)n, (long long)k, sc.grid, sc.dp, sc.sk, sc.ipc, sc.max_seg,
+                   (tend - t0) / 1e3, first / g / 1e3, mainl / g / 1e3, lastml / g / 1e3, fix / g / 1e3,
+                   epi / g / 1e3, units / g, endmin / 1e3, endmax / 1e3);
+    }
+#endif
+  }
+  TB_CUDA(cudaGetLastError(), "kernel launch");
+  return TB_STATUS_OK;
+}
+
+// One persistent launch for the host pipeline's phase 1 (PIPE mode): C =
+// A·B over all k, k-panel q (k-stages [panel_it[q], panel_it[q+1]), panel_it
+// in device memory) consumed once flags[q] != 0. TMA operands (even pitch,
+// 16-byte aligned) only.
+int launch_pipe(int dev, const double* A, int64_t lda, const double* B, int64_t ldb, double* Cm, int64_t ldc,
+                int64_t m, int64_t k, int64_t n, const int* panel_it_d, const int* flags_d, int Q,
+                cudaStream_t stream) {
+  int s = ensure_kernel_attrs(dev);
+  if (s) return s;
+  using Cfg = tb::DmmaCfg;
+  tb::GemmParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.A = A;
+  p.B = B;
+  p.C = Cm;
+  p.lda = lda;
+  p.ldb = ldb;
+  p.ldc = ldc;
+  p.m = (int)m;
+  p.n = (int)n;
+  p.k = (int)k;
+  p.tiles_m = (int)((m + Cfg::BM - 1) / Cfg::BM);
+  p.tiles_n = (int)((n + Cfg::BN - 1) / Cfg::BN);
+  p.num_k = (int)((k + Cfg::BK - 1) / Cfg::BK);
+  p.accumulate = 0;
+  p.vec_store = ((reinterpret_cast<uintptr_t>(Cm) & 15u) == 0 && ldc % 2 == 0) ? 1 : 0;
+  const int64_t tiles = (int64_t)p.tiles_m * p.tiles_n;
+  p.dp_tiles = (int)tiles;
+  p.sk_tiles = Q;                                        // PIPE: panel count
+  p.sk_ipc = 1;
+  p.max_seg = 1;
+  p.counters = const_cast<int*>(panel_it_d);             // PIPE: panel k-stage bounds
+  p.partials = reinterpret_cast<double*>(const_cast<int*>(flags_d));  // PIPE: panel flags
+  if ((s = get_encoder())) return s;
+  CUtensorMap mA, mB;
+  if ((s = encode_map(&mA, A, m, k, lda, Cfg::BM))) return s;
+  if ((s = encode_map(&mB, B, k, n, ldb, Cfg::BK))) return s;
+  void* args[] = {&mA, &mB, &p};
+  const int grid = (int)std::min<int64_t>(tiles, g_dev[dev].sms);
+  TB_CUDA(cudaLaunchKernel(pipe_kernel(), dim3((unsigned)grid), dim3(Cfg::THREADS), args, (size_t)cfg_smem(0), stream),
+          "kernel launch (pipe)");
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return TB_STATUS_OK;
+}
+
+struct EventPair {
+  cudaEvent_t a = nullptr, b = nullptr;
+  ~EventPair() {
+    if (a) cudaEventDestroy(a);
+    if (b) cudaEventDestroy(b);
+  }
+  int create() {
+    TB_CUDA(cudaEventCreate(&a), "event create");
+    TB_CUDA(cudaEventCreate(&b), "event create");
+    return TB_STATUS_OK;
+  }
+};
+
+int timed_gemm(int dev, const double* A, const double* B, double* Cm, int64_t m, int64_t k, int64_t n,
+               int tile_edge, int variant, cudaStream_t stream, double* out_seconds, bool use_cublas) {
+  EventPair ev;
+  int s = ev.create();
+  if (s) return s;
+  TB_CUDA(cudaEventRecord(ev.a, stream), "event record");
+  if (use_cublas) {
+    DeviceState& st = g_dev[dev];
+    {
+      std::lock_guard<std::mutex> lk(st.mu);
+      if (!st.cublas && cublasCreate(&st.cublas) != CUBLAS_STATUS_SUCCESS) {
+        set_err("cublasCreate failed");
+        return TB_STATUS_RUNTIME;
+      }
+    }
+    cublasSetStream(st.cublas, stream);
+    const double one = 1.0, zero = 0.0;
+    // Row-major C = A·B  <=>  column-major C^T = B^T · A^T.
+    if (cublasDgemm(st.cublas, CUBLAS_OP_N, CUBLAS_OP_N, (int)n, (int)m, (int)k, &one, B, (int)n, A, (int)k, &zero,
+                    Cm, (int)n) != CUBLAS_STATUS_SUCCESS) {
+      set_err("cublasDgemm failed");
+      return TB_STATUS_RUNTIME;
+    }
+  } else {
+    s = launch(dev, A, k, B, n, Cm, n, m, k, n, 0, tile_edge, variant, stream);
+    if (s) return s;
+  }
+  TB_CUDA(cudaEventRecord(ev.b, stream), "event record");
+  TB_CUDA(cudaEventSynchronize(ev.b), "kernel execution");
+  float ms = 0.f;
+  TB_CUDA(cudaEventElapsedTime(&ms, ev.a, ev.b), "event elapsed");
+  if (out_seconds) *out_seconds = (double)ms * 1e-3;
+  return TB_STATUS_OK;
+}
+
+int dgemm_common(const double* A, const double* B, double* Cm, int64_t m, int64_t k, int64_t n, int32_t tile_edge,
+                 int32_t variant, int32_t device, void* cuda_stream, double* out_seconds, bool use_cublas) {
+  int s = check_device(device);
+  if (s) return s;
+  if (!A || !B || !Cm || !out_seconds) {
+    set_err("null buffer pointer");
+    return TB_STATUS_BAD_DIMS;
+  }
+  if ((s = validate(m, k, n, tile_edge, variant, device))) return s;
+  DeviceGuard guard(device);
+  return timed_gemm(device, A, B, Cm, m, k, n, tile_edge, variant, static_cast<cudaStream_t>(cuda_stream),
+                    out_seconds, use_cublas);
+}
+
+
+}  // namespace

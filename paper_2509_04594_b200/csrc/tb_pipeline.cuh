@@ -1,0 +1,117 @@
+// tb_pipeline.cuh — the host-buffer pipeline's shape (pure host code,
+// included by tb_capi.cu only; exported as tb_pipeline_plan for tests):
+// phase-1 rows and K-panels, phase-2 row blocks.
+#pragma once
+
+// The host pipeline's shape (pure; exported as tb_pipeline_plan for tests).
+struct PipePlan {
+  int64_t Mq = 0;
+  bool fused = false;          // phase 1 as one PIPE-mode launch
+  std::vector<int64_t> pk;     // phase-1 K-panel bounds
+  std::vector<int64_t> gb;     // phase-1 row groups (one per compute stream)
+  std::vector<int64_t> rb;     // phase-2 row-block bounds, rb[0] = Mq
+};
+
+PipePlan plan_pipeline(int64_t m, int64_t k, int64_t n, int sms, bool fused_ok) {
+  PipePlan pl;
+  int64_t& Mq = pl.Mq;
+  bool& fused = pl.fused;
+  std::vector<int64_t>& pk = pl.pk;
+  std::vector<int64_t>& gb = pl.gb;
+  std::vector<int64_t>& rb = pl.rb;
+  Mq = m;
+  pk = {0, k};
+  gb = {0, m};
+  rb = {m};
+  const double flops = 2.0 * (double)m * (double)n * (double)k;
+  if (flops >= 1e11) {
+    constexpr double kH2D = 55e9, kRate = 36e12;  // B/s (PCIe gen5 x16, measured), flop/s (FP64 DMMA)
+    const double den = (double)n * kH2D - 4.0 * kRate;
+    int64_t mq = den > 0 ? (int64_t)(1.2 * 4.0 * kRate * (double)n / den) : m;
+    int64_t kp0 = 256, kp_max = 2048, blk = 1536, groups = 2;
+    // TB_PIPE=mq,kp0,kp_max,blk[,groups] overrides the shape (tuning experiments).
+    if (const char* e = std::getenv("TB_PIPE")) {
+      long long a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 2;
+      if (std::sscanf(e, "%lld,%lld,%lld,%lld,%lld", &a0, &a1, &a2, &a3, &a4) >= 4 && a0 >= 1 && a1 >= 2 &&
+          a2 >= 2 && a3 >= 1 && a4 >= 1) {
+        mq = a0;
+        kp0 = a1;
+        kp_max = a2;
+        blk = a3;
+        groups = a4;
+      }
+    }
+    mq = (mq + 127) / 128 * 128;
+    // Phase 1 as one persistent launch that waits on per-panel flags (PIPE
+    // mode) rather than a launch per panel and row group; TB_PIPE_FUSED=0
+    // restores the launch-per-panel form (A/B).
+    const char* fe = std::getenv("TB_PIPE_FUSED");
+    fused = fused_ok && !(fe && std::strcmp(fe, "0") == 0);
+    if (fused && !std::getenv("TB_PIPE")) {
+      // The fused launch gives CTA c the phase-1 tiles c, c + P, ...: pick
+      // the tile-row count (>= the compute-cover minimum, up to 8 more) whose
+      // tile count leaves the least imbalance, ceil(T/P) - T/P (N = 10000:
+      // 34 rows -> 18.15 tiles per CTA, 59.1 ms; 41 rows -> 21.89, 58.0 ms;
+      // profiles/r01_pipe_trace_mq_sweep.txt).
+      const int64_t tn = (n + 127) / 128, P_sm = sms;
+      int64_t best_r = mq / 128;
+      double best_imb = 2.0;
+      for (int64_t rr = mq / 128; rr <= mq / 128 + 8 && rr * 128 < m - blk / 2; ++rr) {
+        const double per = (double)(rr * tn) / (double)P_sm;
+        const double imb = std::ceil(per) - per;
+        if (imb < best_imb - 1e-9) {
+          best_imb = imb;
+          best_r = rr;
+        }
+      }
+      mq = best_r * 128;
+    }
+    Mq = mq >= m - blk / 2 ? m : mq;
+    const int64_t kal = fused ? 16 : 2;  // panel bounds on k-stage (PIPE) or TMA (even k0) boundaries
+    // Panel sizes: after a small first panel, each panel is as large as can
+    // land (transfer model) before the GEMMs queued so far drain (compute
+    // model), so the panels grow geometrically by the compute/transfer ratio
+    // without opening a compute gap; capped at kp_max.
+    const double tr_per_k = 8.0 * (double)(Mq + n) / kH2D, c_per_k = 2.0 * (double)Mq * (double)n / kRate;
+    pk.assign(1, 0);
+    double arrive = 0.0, finish = 0.0;
+    for (int64_t at = 0, step = kp0; at < k;) {
+      int64_t nx = at + step >= k - step / 2 ? k : ((at + step) / kal * kal);
+      if (nx <= at) nx = std::min<int64_t>(k, at + kal);
+      arrive += tr_per_k * (double)(nx - at);
+      finish = std::max(finish, arrive) + c_per_k * (double)(nx - at);
+      pk.push_back(nx);
+      at = nx;
+      step = std::min<int64_t>(kp_max, std::max<int64_t>(kp0, (int64_t)((finish - arrive) / tr_per_k)));
+    }
+    gb = (groups >= 2 && Mq >= 2048) ? std::vector<int64_t>{0, (Mq / 2 + 127) / 128 * 128, Mq}
+                                     : std::vector<int64_t>{0, Mq};
+    int64_t r = m - Mq;
+    std::vector<int64_t> tail;
+    for (int64_t t : {std::min<int64_t>(128, blk / 4), blk / 2})  // shrinking tail: the last D2H is ~10-20 MB
+      if (t > 0 && r >= 2 * t) {
+        tail.push_back(t);
+        r -= t;
+      }
+    rb.assign(1, Mq);
+    const int64_t nb = (r + blk - 1) / blk;
+    // Block bounds on 128-row tile boundaries: a block of, say, 1413 rows
+    // would pad its last tile row to 1536 (8 % of its DMMAs on zeros).
+    for (int64_t i = 1; i <= nb; ++i) {
+      const int64_t bnd = i == nb ? Mq + r : std::min(Mq + r, Mq + (r * i / nb + 64) / 128 * 128);
+      if (bnd > rb.back()) rb.push_back(bnd);  // no empty blocks
+    }
+    for (auto it = tail.rbegin(); it != tail.rend(); ++it) rb.push_back(rb.back() + *it);
+    // Interior bounds on tile rows (Mq is a multiple of 128): only the last
+    // block may be ragged.
+    std::vector<int64_t> al{rb.front()};
+    for (size_t i = 1; i + 1 < rb.size(); ++i) {
+      const int64_t v = (rb[i] + 64) / 128 * 128;
+      if (v > al.back() && v < m) al.push_back(v);
+    }
+    if (m > al.back()) al.push_back(m);
+    rb.swap(al);
+  }
+  if (pl.pk.size() - 1 < 2 || pl.pk.size() - 1 > 120) pl.fused = false;  // table holds <= 120 panels
+  return pl;
+}

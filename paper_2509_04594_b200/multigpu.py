@@ -21,7 +21,7 @@ from typing import Callable
 import torch
 import torch.distributed as dist
 
-__all__ = ["row_partitions", "panel_bounds", "gathered_panels", "ShardedGemm", "HostShardedGemm", "gather_rows"]
+__all__ = ["row_partitions", "panel_bounds", "ramp_panel_bounds", "gathered_panels", "ShardedGemm", "HostShardedGemm", "gather_rows"]
 
 
 def row_partitions(m: int, world: int) -> list[tuple[int, int]]:
@@ -53,6 +53,19 @@ def panel_bounds(k: int, panels: int) -> list[tuple[int, int]]:
         out.append((k0, k1))
         k0 = k1
     return out
+
+
+def ramp_panel_bounds(k: int, panels: int) -> list[tuple[int, int]]:
+    """``panel_bounds`` with a short first panel: only panel 0's broadcast is
+    exposed before the first GEMM (each later panel's broadcast hides under
+    the previous panel's GEMM — NVLink moves a B panel ~4x faster than a
+    1250-row shard multiplies it), so it is 1/8 of an even panel."""
+    even = panel_bounds(k, panels)
+    if len(even) < 2:
+        return even
+    first = max(2, ((even[0][1] - even[0][0]) // 8) & ~1)
+    rest = panel_bounds(k - first, max(1, len(even) - 1))
+    return [(0, first)] + [(first + a, first + b) for a, b in rest]
 
 
 def gathered_panels(k: int, world: int, panels: int) -> list[tuple[int, int]]:
@@ -98,7 +111,7 @@ class ShardedGemm:
             raise ValueError(f"shapes {tuple(a_local.shape)} @ {tuple(b.shape)} -> {tuple(out_local.shape)}")
         if not b.is_contiguous():
             raise ValueError("b must be contiguous (row-major)")
-        bounds = panel_bounds(b.shape[0], self.panels)
+        bounds = ramp_panel_bounds(b.shape[0], self.panels)
         if len(bounds) == 1:
             dist.broadcast(b, self.src, group=self.group)
             if a_local.shape[0] > 0:

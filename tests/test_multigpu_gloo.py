@@ -12,7 +12,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from paper_2509_04594_b200.multigpu import (HostShardedGemm, ShardedGemm, gather_rows, gathered_panels, panel_bounds,
-                                            row_partitions)
+                                            ramp_panel_bounds, row_partitions)
 
 
 def _free_port():
@@ -132,3 +132,13 @@ def test_gathered_panels_cover_and_divide():
                 assert b[0][0] == 0 and b[-1][1] >= k and b[-1][1] - k < 2 * world
                 assert all(x1 == y0 for (_, x1), (y0, _) in zip(b, b[1:]))
                 assert all((k1 - k0) % (2 * world) == 0 and k1 > k0 for k0, k1 in b)
+
+
+def test_ramp_panel_bounds():
+    for k in (1, 2, 3, 5, 37, 1000, 10000, 32768):
+        for panels in (1, 2, 4, 7):
+            b = ramp_panel_bounds(k, panels)
+            assert b[0][0] == 0 and b[-1][1] == k and all(x1 == y0 for (_, x1), (y0, _) in zip(b, b[1:]))
+            assert all(k1 > k0 and k0 % 2 == 0 for k0, k1 in b)
+            if len(b) > 2 and k >= 1000:
+                assert b[0][1] - b[0][0] <= (b[1][1] - b[1][0]) // 4  # short first panel

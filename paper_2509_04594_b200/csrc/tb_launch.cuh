@@ -105,8 +105,7 @@ int split_workspace(int dev, cudaStream_t stream, size_t partial_elems, size_t c
   return TB_STATUS_OK;
 }
 
-// Enqueue one GEMM on `stream` (current device = dev). Assumes validated args.
-// AUTO on operands TMA cannot address (odd leading dimension or a base not
+// Staging. AUTO on operands TMA cannot address (odd leading dimension or a base not
 // 16-byte aligned — the reference's odd-N cases) would run the cp.async
 // loader at ~92 % of the TMA path's speed. For large products the operands
 // are instead copied once, on the launching stream, into even-pitch

@@ -161,6 +161,27 @@ def cpu_sample(n: int, threads: int, rows: int) -> dict:
             "seconds": dt}
 
 
+def blas_sample(n: int, target_s: float = 3.0) -> dict:
+    """The reference's BLAS backend (``a @ b`` through numpy's bundled
+    OpenBLAS, demos/06_external_backends.py / SURVEY.md §8(d)) on a row
+    sample of the N x N product, all host threads: reported beside the
+    tiled-path baseline, not the reference arm's value."""
+    import numpy as np
+
+    a_full, b = _cpu_operands(n, 256)
+    t0 = time.perf_counter()
+    a_full @ b
+    dt = max(time.perf_counter() - t0, 1e-3)
+    rows = int(min(n, max(256, 256 * target_s / dt)))
+    a, _ = _cpu_operands(n, rows) if rows > 256 else (a_full, b)
+    t0 = time.perf_counter()
+    a @ b
+    dt = time.perf_counter() - t0
+    threads = os.environ.get("OPENBLAS_NUM_THREADS") or os.cpu_count()
+    return {"value": rows * (2 * n * n - n) / dt / 1e9, "unit": UNIT, "threads": threads,
+            "sample": f"numpy {np.__version__} matmul (OpenBLAS) on {rows} of {n} rows, {dt:.2f} s"}
+
+
 def run_reference(args) -> None:
     rank, world, _ = env_rank()
     if rank != 0:
@@ -177,7 +198,8 @@ def run_reference(args) -> None:
             "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic uniform[2,5] (numpy PCG64)",
             "config": {"workload": f"N={args.n} FP64 square GEMM, bounded row sample on host cores", "n": args.n},
-            "cpu_baseline": {**{k: vals[-1][k] for k in ("unit", "cores", "kind", "sample")}, "value": v},
+            "cpu_baseline": {**{k: vals[-1][k] for k in ("unit", "cores", "kind", "sample")}, "value": v,
+                             "blas": blas_sample(args.n)},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "ms_per_step": statistics.median([s["seconds"] for s in vals]) * 1e3}
     print(json.dumps(line), flush=True)
@@ -344,6 +366,7 @@ def run_ours(args) -> None:
         threads = os.cpu_count() or 1
         cpu = cpu_sample(n, threads, cpu_calibrate(n, threads, args.ref_seconds))
         cpu.pop("seconds", None)
+        cpu["blas"] = blas_sample(n)
 
     if rank == 0:
         line = {

@@ -184,8 +184,22 @@ def gpu_tiled_multiply_timed(a, b, tile: TileConfig = TileConfig(), variant="aut
 
 
 def gpu_tiled_multiply(a, b, tile: TileConfig = TileConfig(), variant="auto", device=None) -> np.ndarray:
-    """``MultiplyFn`` form (backends.py:56): fresh product, inputs untouched."""
-    return gpu_tiled_multiply_timed(a, b, tile, variant, device)[0]
+    """``MultiplyFn`` form (backends.py:56): fresh product, inputs untouched.
+
+    The reference harness times this call end to end (harness.py:163-172),
+    so it goes through the host-buffer entry: its copy/compute pipeline
+    stages the caller's pageable numpy arrays through pinned slots and
+    overlaps the copies with the GEMM (N = 10000: 567 ms through plain
+    upload + GEMM + download before). Kernel-only seconds for FLOPS records
+    come from ``gpu_tiled_multiply_timed``."""
+    a, b = require_operands(a, b)
+    tile.validate()
+    m, k = a.shape
+    n = b.shape[1]
+    out = np.empty((m, n), dtype=np.float64)
+    sec = np.zeros(1)
+    _lib.check(gpu_tiled_multiply_flat(_device_index(device), a, b, m, k, n, tile.k, out, sec, variant=variant))
+    return out
 
 
 def cublas_multiply_timed(a, b, device=None):

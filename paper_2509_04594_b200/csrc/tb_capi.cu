@@ -32,6 +32,7 @@
 #include "tb_state.cuh"
 #include "tb_launch.cuh"
 #include "tb_pipeline.cuh"
+#include "tb_staging.cuh"
 
 extern "C" {
 
@@ -132,6 +133,18 @@ int tb_gpu_tiled_multiply_flat_ex(int32_t device, const double* a, const double*
   double* dC = dB + up(nb);
   const cudaStream_t hs = st.h2d_stream, ds = st.d2h_stream;
   const cudaStream_t css[2] = {st.host_stream, st.host_stream2};
+  // Pageable operands / output go through the pinned staging ring
+  // (tb_staging.cuh); TB_STAGE=0 keeps plain pageable copies (A/B).
+  const bool stage_ok = !(std::getenv("TB_STAGE") && std::strcmp(std::getenv("TB_STAGE"), "0") == 0);
+  const bool pin_a = is_pinned(a), pin_b = is_pinned(b), pin_c = is_pinned(out_c);
+  const bool stage_a = stage_ok && !pin_a, stage_b = stage_ok && !pin_b, stage_c = stage_ok && !pin_c;
+  // A plain pageable cudaMemcpyAsync blocks the host (and can wait on device
+  // work), so it must not be issued behind the flag-spinning fused phase-1
+  // launch: without staging, pageable buffers take the event-gated
+  // launch-per-panel form.
+  const bool direct_pageable = !(pin_a || stage_a) || !(pin_b || stage_b) || !(pin_c || stage_c);
+  StageRing& ring = g_ring[device];
+  if ((stage_a || stage_b || stage_c) && (s = ring.ensure())) return s;
 
   // Copy/compute/copy pipeline over four streams (H2D, two compute, D2H).
   //  Phase 1 (rank-k panels): the first Mq rows of C are computed as
@@ -145,7 +158,8 @@ int tb_gpu_tiled_multiply_flat_ex(int32_t device, const double* a, const double*
   //  once, and the last blocks shrink so the final D2H is short.
   // Small problems degenerate to copy, GEMM, copy.
   const bool fused_ok = variant != TB_VARIANT_PAPER && variant != TB_VARIANT_DFMA &&
-                        variant != TB_VARIANT_DMMA_CPASYNC && cfg_smem(0) <= g_dev[device].smem_optin;
+                        variant != TB_VARIANT_DMMA_CPASYNC && cfg_smem(0) <= g_dev[device].smem_optin &&
+                        !direct_pageable;
   const PipePlan plan = plan_pipeline(m, k, n, g_dev[device].sms, fused_ok);
   const int64_t Mq = plan.Mq;
   bool fused = plan.fused;
@@ -214,7 +228,24 @@ int tb_gpu_tiled_multiply_flat_ex(int32_t device, const double* a, const double*
                  int64_t c1, const char* what, int idx) -> int {
     cudaEvent_t t0 = trace_begin(hs);
     const size_t pitch = (size_t)cols * sizeof(double);
-    if (c0 == 0 && c1 == cols && dld == cols)
+    if ((src == a && stage_a) || (src == b && stage_b)) {
+      // Pageable source: fill pinned slots on the host (pool threads), then
+      // DMA each slot; a slot is refilled once its previous copy completed.
+      const size_t w = (size_t)(c1 - c0) * sizeof(double);
+      const int64_t rows_per = std::max<int64_t>(1, (int64_t)(StageRing::kSlotBytes / w));
+      for (int64_t r = r0; r < r1; r += rows_per) {
+        const int64_t nr = std::min(rows_per, r1 - r);
+        const int i = ring.next;
+        ring.next = (ring.next + 1) % StageRing::kSlots;
+        TB_CUDA(cudaEventSynchronize(ring.ev[i]), "staging slot wait");
+        pool_copy_rows(*ring.pool, ring.slot[i], w, reinterpret_cast<const char*>(src + r * cols + c0), pitch, w,
+                       (size_t)nr);
+        TB_CUDA(cudaMemcpy2DAsync(dst + r * dld + c0, (size_t)dld * sizeof(double), ring.slot[i], w, w, (size_t)nr,
+                                  cudaMemcpyHostToDevice, hs),
+                "host to device copy");
+        TB_CUDA(cudaEventRecord(ring.ev[i], hs), "event record");
+      }
+    } else if (c0 == 0 && c1 == cols && dld == cols)
       TB_CUDA(cudaMemcpyAsync(dst + r0 * cols, src + r0 * cols, (size_t)(r1 - r0) * pitch, cudaMemcpyHostToDevice,
                               hs),
               "host to device copy");
@@ -238,11 +269,22 @@ int tb_gpu_tiled_multiply_flat_ex(int32_t device, const double* a, const double*
     return TB_STATUS_OK;
   };
   int nd2h = 0;
-  // Rows [r0, r1) x columns [c0, c1) of C back to the host, after `cs`'s work so far.
+  // Rows [r0, r1) x columns [c0, c1) of C back to the host, after `cs`'s work
+  // so far. A pageable output is drained through the staging ring at the end
+  // of the enqueue (drain_c).
+  struct D2HJob {
+    cudaEvent_t ready;
+    int64_t r0, r1, c0, c1;
+  };
+  std::vector<D2HJob> djobs;
   auto d2h = [&](cudaStream_t cs, int64_t r0, int64_t r1, int64_t c0, int64_t c1) -> int {
     cudaEvent_t done = mk(cudaEventDisableTiming);
     if (!done) return cuda_fail(cudaGetLastError(), "event create");
     TB_CUDA(cudaEventRecord(done, cs), "event record");
+    if (stage_c) {
+      djobs.push_back({done, r0, r1, c0, c1});
+      return TB_STATUS_OK;
+    }
     TB_CUDA(cudaStreamWaitEvent(ds, done, 0), "stream wait");
     cudaEvent_t t0 = trace_begin(ds);
     if (ldc_d == n && c0 == 0 && c1 == n)
@@ -279,20 +321,11 @@ int tb_gpu_tiled_multiply_flat_ex(int32_t device, const double* a, const double*
     if (!(evTab = mk(cudaEventDisableTiming))) return cuda_fail(cudaGetLastError(), "event create");
     TB_CUDA(cudaEventRecord(evTab, hs), "event record");
   }
-  // H2D: phase-1 panels (A slice, then B rows; in fused mode then the
-  // panel's flag, copied after its data on the same stream), then the
-  // phase-2 row blocks.
-  for (int p = 0; p < P; ++p) {
-    if (Mq > 0 && (s = h2d(dA, lda_d, a, k, 0, Mq, pk[p], pk[p + 1], "h2d_Ap", p))) return s;
-    if ((s = h2d(dB, ldb_d, b, n, pk[p], pk[p + 1], 0, n, "h2d_Bp", p))) return s;
-    TB_CUDA(cudaEventRecord(evP[p], hs), "event record");
-    if (fused)
-      TB_CUDA(cudaMemcpyAsync(st.dtab + p, st.htab + 256, sizeof(int), cudaMemcpyHostToDevice, hs), "panel flag");
-  }
-  for (int r = 0; r < R; ++r) {
-    if ((s = h2d(dA, lda_d, a, k, rb[r], rb[r + 1], 0, k, "h2d_A", r))) return s;
-    TB_CUDA(cudaEventRecord(evA[r], hs), "event record");
-  }
+  // Enqueue in data order, so that host-staged copies (which block this
+  // thread while it fills pinned slots) never delay compute that could run:
+  // the fused phase-1 launch first (its flags gate it), then per K-panel the
+  // copies (+ the unfused form's panel GEMMs), then per row block its copy
+  // and GEMM; the column strip once all of A has been enqueued.
   if (fused) {
     // Phase 1: one persistent launch; its producer waits on each panel's flag.
     const cudaStream_t cs = css[0];
@@ -305,21 +338,28 @@ int tb_gpu_tiled_multiply_flat_ex(int32_t device, const double* a, const double*
     if ((s = launch_pipe(device, dA, lda_d, dB, ldb_d, dC, ldc_d, Mq, k, n1, st.dtab + 128, st.dtab, P, cs))) return s;
     TB_CUDA(cudaEventRecord(t1, cs), "event record");
     if ((s = d2h(cs, 0, Mq, 0, n1))) return s;
-  } else {
-    // Phase 1: panel p of every row group once it has landed; row group g
-    // stays on stream g, so its partial sums accumulate in panel order.
-    for (int p = 0; p < P; ++p)
+  }
+  // H2D of phase-1 panels: A slice, then B rows; in fused mode then the
+  // panel's flag, copied after its data on the same stream.
+  for (int p = 0; p < P; ++p) {
+    if (Mq > 0 && (s = h2d(dA, lda_d, a, k, 0, Mq, pk[p], pk[p + 1], "h2d_Ap", p))) return s;
+    if ((s = h2d(dB, ldb_d, b, n, pk[p], pk[p + 1], 0, n, "h2d_Bp", p))) return s;
+    TB_CUDA(cudaEventRecord(evP[p], hs), "event record");
+    if (fused) {
+      TB_CUDA(cudaMemcpyAsync(st.dtab + p, st.htab + 256, sizeof(int), cudaMemcpyHostToDevice, hs), "panel flag");
+    } else {
+      // Phase 1, unfused: panel p of every row group once it has landed; row
+      // group g stays on stream g, so its partial sums accumulate in panel order.
       for (int g = 0; g < G; ++g) {
         TB_CUDA(cudaStreamWaitEvent(css[g], evP[p], 0), "stream wait");
         if ((s = gemm(css[g], gb[g], gb[g + 1], pk[p], pk[p + 1], p > 0))) return s;
         if (p == P - 1 && (s = d2h(css[g], gb[g], gb[g + 1], 0, n1))) return s;
       }
+    }
   }
-  // Phase 2: full-K row blocks, alternating streams (the first one on the
-  // stream the fused phase-1 launch does not hold).
-  // The column strip needs all of A and B; it is enqueued after the block
-  // two from the end, on that block's stream, so it overlaps the last blocks
-  // instead of trailing them.
+  // The column strip needs all of A and B; it goes on the stream the last
+  // row block does not use, after the block before it, so it overlaps the
+  // last block instead of trailing it.
   auto strip = [&](cudaStream_t cs) -> int {
     if (R > 0) TB_CUDA(cudaStreamWaitEvent(cs, evA[R - 1], 0), "stream wait");
     TB_CUDA(cudaStreamWaitEvent(cs, evP[P - 1], 0), "stream wait");
@@ -334,17 +374,59 @@ int tb_gpu_tiled_multiply_flat_ex(int32_t device, const double* a, const double*
     TB_CUDA(cudaEventRecord(t1, cs), "event record");
     return d2h(cs, 0, m, n1, n);
   };
-  const int strip_after = std::max(0, R - 3);
   if (strip_n && R == 0 && (s = strip(css[1]))) return s;
+  // Phase 2: full-K row blocks, alternating streams (the first one on the
+  // stream the fused phase-1 launch does not hold).
   for (int r = 0; r < R; ++r) {
+    if ((s = h2d(dA, lda_d, a, k, rb[r], rb[r + 1], 0, k, "h2d_A", r))) return s;
+    TB_CUDA(cudaEventRecord(evA[r], hs), "event record");
     const cudaStream_t cs = css[(r + (fused ? 1 : 0)) & 1];
+    if (strip_n && r == R - 1 && (s = strip(css[(r + (fused ? 1 : 0) + 1) & 1]))) return s;
     TB_CUDA(cudaStreamWaitEvent(cs, evP[P - 1], 0), "stream wait");
     TB_CUDA(cudaStreamWaitEvent(cs, evA[r], 0), "stream wait");
     if ((s = gemm(cs, rb[r], rb[r + 1], 0, k, false))) return s;
     if ((s = d2h(cs, rb[r], rb[r + 1], 0, n1))) return s;
-    if (strip_n && r == strip_after && (s = strip(cs))) return s;
   }
-  TB_CUDA(cudaEventRecord(e_end, ds), "event record");
+  // Pageable output: drain C through the staging ring, in job order; up to
+  // kSlots D2H copies in flight while the host copies finished slots out.
+  if (stage_c) {
+    struct Pending {
+      int slot;
+      double* dst;
+      size_t w;
+      int64_t rows;
+    };
+    std::vector<Pending> inflight;  // FIFO (front = oldest)
+    size_t head = 0;
+    auto pop = [&]() -> int {
+      const Pending& pd = inflight[head++];
+      TB_CUDA(cudaEventSynchronize(ring.ev[pd.slot]), "device to host copy");
+      pool_copy_rows(*ring.pool, reinterpret_cast<char*>(pd.dst), (size_t)n * sizeof(double), ring.slot[pd.slot],
+                     pd.w, pd.w, (size_t)pd.rows);
+      return TB_STATUS_OK;
+    };
+    for (const D2HJob& jb : djobs) {
+      TB_CUDA(cudaStreamWaitEvent(ds, jb.ready, 0), "stream wait");
+      const size_t w = (size_t)(jb.c1 - jb.c0) * sizeof(double);
+      const int64_t rows_per = std::max<int64_t>(1, (int64_t)(StageRing::kSlotBytes / w));
+      for (int64_t r = jb.r0; r < jb.r1; r += rows_per) {
+        const int64_t nr = std::min(rows_per, jb.r1 - r);
+        if (inflight.size() - head == (size_t)StageRing::kSlots && (s = pop())) return s;
+        const int i = ring.next;
+        ring.next = (ring.next + 1) % StageRing::kSlots;
+        TB_CUDA(cudaStreamWaitEvent(ds, ring.ev[i], 0), "stream wait");  // the slot's last H2D has read it
+        TB_CUDA(cudaMemcpy2DAsync(ring.slot[i], w, dC + r * ldc_d + jb.c0, (size_t)ldc_d * sizeof(double), w,
+                                  (size_t)nr, cudaMemcpyDeviceToHost, ds),
+                "device to host copy");
+        TB_CUDA(cudaEventRecord(ring.ev[i], ds), "event record");
+        inflight.push_back({i, out_c + r * n + jb.c0, w, nr});
+      }
+    }
+    TB_CUDA(cudaEventRecord(e_end, ds), "event record");
+    while (head < inflight.size())
+      if ((s = pop())) return s;
+  }
+  if (!stage_c) TB_CUDA(cudaEventRecord(e_end, ds), "event record");
   const auto h_enq = std::chrono::steady_clock::now();
   // The call is synchronous: spin on the last D2H's event rather than a
   // blocking wait, whose wake-up latency would add to every call.
@@ -432,6 +514,7 @@ void tb_release(void) {
       if (*sp) cudaStreamDestroy(*sp);
       *sp = nullptr;
     }
+    g_ring[d].release();
     if (st.dtab) cudaFree(st.dtab);
     if (st.htab) cudaFreeHost(st.htab);
     st.dtab = nullptr;

@@ -413,6 +413,49 @@ def test_staged_tma_for_misaligned_operands(tb, oracle):
     assert (torch.linalg.norm(out - ref) / torch.linalg.norm(ref)).item() <= NORMWISE
 
 
+@pytest.mark.parametrize("m,k,n", [(4000, 4000, 4032), (333, 129, 257), (7001, 3000, 5000)])
+def test_pageable_staging_matches_direct_copies(tb, oracle, monkeypatch, m, k, n):
+    """Pageable (numpy) host buffers go through the pinned staging ring and
+    the copy-thread pool; the product matches the plain pageable copies
+    (TB_STAGE=0, which also takes the launch-per-panel phase 1, so a
+    different k-split: normwise) and is bitwise the same when a pinned output
+    with pageable inputs (and the reverse) mixes both paths."""
+    import torch
+
+    a, b = oracle.generate(m, k, 51), oracle.generate(k, n, 52)
+    s = np.zeros(1)
+    outs = []
+    for stage in ("1", "0"):
+        monkeypatch.setenv("TB_STAGE", stage)
+        c = np.full(m * n, np.nan)
+        assert tb.gpu_tiled_multiply_flat(0, a, b, m, k, n, 32, c, s) == tb.STATUS_OK
+        outs.append(c)
+    assert oracle.normwise_rel(outs[0].reshape(m, n), outs[1].reshape(m, n)) <= NORMWISE
+    monkeypatch.setenv("TB_STAGE", "1")
+    c_pin = torch.full((m, n), float("nan"), dtype=torch.float64).pin_memory()
+    assert tb.gpu_tiled_multiply_flat(0, a, b, m, k, n, 32, c_pin, s) == tb.STATUS_OK
+    assert np.array_equal(c_pin.numpy().ravel(), outs[0])
+    a_pin = torch.from_numpy(a).pin_memory()
+    c = np.full(m * n, np.nan)
+    assert tb.gpu_tiled_multiply_flat(0, a_pin, b, m, k, n, 32, c, s) == tb.STATUS_OK
+    assert np.array_equal(c, outs[0])
+    rows = np.r_[0:2, m - 2:m]
+    assert oracle.normwise_rel(outs[0].reshape(m, n)[rows], oracle.tiled_parallel(a[rows], b)) <= NORMWISE
+
+
+def test_multiplyfn_through_host_pipeline(tb, oracle):
+    """The registered MultiplyFn (what the reference harness times) returns a
+    fresh product equal to the oracle, inputs untouched."""
+    for m, k, n in ((1000, 1000, 1000), (2501, 1999, 3003)):
+        a, b = oracle.generate(m, k, 61), oracle.generate(k, n, 62)
+        a0, b0 = a.copy(), b.copy()
+        c = tb.gpu_tiled_multiply(a, b)
+        assert c.shape == (m, n) and c.dtype == np.float64
+        assert np.array_equal(a, a0) and np.array_equal(b, b0)
+        rows = np.r_[0:3, m - 3:m]
+        assert oracle.normwise_rel(c[rows], oracle.tiled_parallel(a[rows], b)) <= NORMWISE
+
+
 def test_concurrent_host_threads(tb, oracle):
     """The registered MultiplyFn and the flat host entry called from several
     host threads at once (the reference's CPU backends are thread-safe,

@@ -196,6 +196,10 @@ def gpu_tiled_multiply(a, b, tile: TileConfig = TileConfig(), variant="auto", de
     tile.validate()
     m, k = a.shape
     n = b.shape[1]
+    if 2.0 * m * n * k < 1e10:
+        # small products: a plain upload / launch / download is quicker than
+        # staging (N = 1000: 1.5 vs 2.2 ms; N = 2000: 7.5 vs 5.3 ms)
+        return gpu_tiled_multiply_timed(a, b, tile, variant, device)[0]
     out = np.empty((m, n), dtype=np.float64)
     sec = np.zeros(1)
     _lib.check(gpu_tiled_multiply_flat(_device_index(device), a, b, m, k, n, tile.k, out, sec, variant=variant))

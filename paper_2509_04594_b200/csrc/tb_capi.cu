@@ -441,11 +441,20 @@ int tb_gpu_tiled_multiply_flat_ex(int32_t device, const double* a, const double*
   }
   for (cudaStream_t cs : css) TB_CUDA(cudaStreamSynchronize(cs), "kernel execution");
   const auto h_sync = std::chrono::steady_clock::now();
-  double ksum = 0.0;
+  // Kernel-only seconds (outSeconds): the union of the GEMM launches'
+  // intervals — launches on the two compute streams overlap, so their sum
+  // would count shared time twice.
+  std::vector<std::pair<float, float>> iv(kt0.size());
   for (size_t i = 0; i < kt0.size(); ++i) {
-    float ms = 0.f;
-    TB_CUDA(cudaEventElapsedTime(&ms, kt0[i], kt1[i]), "event elapsed");
-    ksum += ms;
+    TB_CUDA(cudaEventElapsedTime(&iv[i].first, e_start, kt0[i]), "event elapsed");
+    TB_CUDA(cudaEventElapsedTime(&iv[i].second, e_start, kt1[i]), "event elapsed");
+  }
+  std::sort(iv.begin(), iv.end());
+  double ksum = 0.0, cover = -1e30;
+  for (const auto& x : iv) {
+    const double lo = std::max<double>(x.first, cover);
+    if (x.second > lo) ksum += x.second - lo;
+    cover = std::max<double>(cover, x.second);
   }
   float e_ms = 0.f;
   TB_CUDA(cudaEventElapsedTime(&e_ms, e_start, e_end), "event elapsed");
@@ -464,7 +473,7 @@ int tb_gpu_tiled_multiply_flat_ex(int32_t device, const double* a, const double*
       std::fprintf(stderr, "TBTRACE %s %d %.4f %.4f %.0f\n", t.what, t.idx, a0, a1, t.bytes);
     }
   }
-  *out_seconds = ksum * 1e-3;  // kernel-only: sum of the GEMM launch durations
+  *out_seconds = ksum * 1e-3;
   if (out_e2e_seconds) *out_e2e_seconds = (double)e_ms * 1e-3;
   return TB_STATUS_OK;
 }

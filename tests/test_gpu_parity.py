@@ -456,6 +456,29 @@ def test_multiplyfn_through_host_pipeline(tb, oracle):
         assert oracle.normwise_rel(c[rows], oracle.tiled_parallel(a[rows], b)) <= NORMWISE
 
 
+def test_flat_repeated_varied_calls(tb, oracle):
+    """Back-to-back host-buffer calls of varying size and buffer kind (pinned
+    / pageable, pipelined / single-shot, ragged / aligned) reuse and regrow
+    the cached workspaces, event pool, staging ring and pipeline tables:
+    every result equals cuBLAS on the same operands."""
+    import torch
+
+    rng = np.random.default_rng(7)
+    shapes = [(4000, 4000, 4032), (700, 300, 900), (5003, 2999, 4500), (128, 64, 128), (4100, 4000, 4000),
+              (6000, 3000, 2000), (333, 1000, 77)]
+    for i, (m, k, n) in enumerate(shapes * 2):
+        a = rng.random((m, k)) * 3 + 2
+        b = rng.random((k, n)) * 3 + 2
+        pinned = i % 3 == 0
+        ah = torch.from_numpy(a).pin_memory() if pinned else a
+        bh = torch.from_numpy(b).pin_memory() if i % 2 == 0 else b
+        c = torch.empty((m, n), dtype=torch.float64).pin_memory() if pinned else np.empty(m * n)
+        assert tb.gpu_tiled_multiply_flat(0, ah, bh, m, k, n, 32, c, np.zeros(1)) == tb.STATUS_OK
+        got = torch.as_tensor(np.asarray(c).reshape(m, n)).cuda()
+        ref, _ = tb.cublas_dgemm(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda())
+        assert (torch.linalg.norm(got - ref) / torch.linalg.norm(ref)).item() <= NORMWISE, (m, k, n, i)
+
+
 def test_concurrent_host_threads(tb, oracle):
     """The registered MultiplyFn and the flat host entry called from several
     host threads at once (the reference's CPU backends are thread-safe,

@@ -252,7 +252,7 @@ int launch_tiles(int dev, const double* A, int64_t lda, const double* B, int64_t
     p.n = (int)n;
     p.k = (int)k;
     const bool dfma = variant == TB_VARIANT_DFMA;
-    const StripInfo si = strip > 0 ? strip_info(strip) : StripInfo{0, 0, nullptr, 0};
+    const StripInfo si = strip > 0 ? strip_info(strip) : StripInfo{0, 0, 1, nullptr, 0};
     const bool narrow = si.fn != nullptr;  // an edge-strip shape (TMA only)
     const int bm = narrow ? si.bm : strip == kStrip64x128 ? 64 : strip < 0 ? 128 : choose_bm(m, n, g_dev[dev].sms, dfma);
     const int bn = narrow ? si.bn : Cfg::BN;
@@ -266,7 +266,8 @@ int launch_tiles(int dev, const double* A, int64_t lda, const double* B, int64_t
       return TB_STATUS_OVER_LIMITS;
     }
     const int cfg = dfma ? 0 : active_cfg();
-    const int64_t kstage = (bm == 64 || narrow) ? (int64_t)Cfg::BK : (int64_t)Cfg::BK * kCfgs[cfg].sub;
+    const int64_t kstage = narrow ? (int64_t)Cfg::BK * si.sub : bm == 64 ? (int64_t)Cfg::BK
+                                                                       : (int64_t)Cfg::BK * kCfgs[cfg].sub;
     p.num_k = (int)((k + kstage - 1) / kstage);
     const Schedule sc = plan_schedule(tiles, p.num_k, g_dev[dev].sms);
     p.num_k = sc.num_k;  // split-K pads the k-slab count (extra slabs read as zeros)

@@ -77,27 +77,28 @@ enum StripCfg : int {
   kStrip32x128,
   kStrip64x128
 };
-constexpr int kStripStages = 8;
-template <int BM, int BN, int WM>
+// Narrow tiles do little work per 16-deep k-slab, so a strip stage holds
+// several sub-slabs (SUB x 16 k) to amortise the per-stage barrier round trip.
+template <int BM, int BN, int WM, int SUB, int STAGES>
 struct StripK {
   static void* fn() {
-    return (void*)tb::dgemm_dmma_kernel<1, kStripStages, tb::Loader::TMA, tb::Math::DMMA, BM, false, BN, WM>;
+    return (void*)tb::dgemm_dmma_kernel<SUB, STAGES, tb::Loader::TMA, tb::Math::DMMA, BM, false, BN, WM>;
   }
-  static constexpr int smem() { return tb::dmma_smem_bytes<1, kStripStages, BM, BN>(); }
+  static constexpr int smem() { return tb::dmma_smem_bytes<SUB, STAGES, BM, BN>(); }
 };
 struct StripInfo {
-  int bm, bn;
+  int bm, bn, sub;
   void* fn;
   int smem;
 };
 StripInfo strip_info(int c) {
   switch (c) {
-    case kStrip128x16: return {128, 16, StripK<128, 16, 8>::fn(), StripK<128, 16, 8>::smem()};
-    case kStrip128x32: return {128, 32, StripK<128, 32, 8>::fn(), StripK<128, 32, 8>::smem()};
-    case kStrip128x64: return {128, 64, StripK<128, 64, 4>::fn(), StripK<128, 64, 4>::smem()};
-    case kStrip16x128: return {16, 128, StripK<16, 128, 1>::fn(), StripK<16, 128, 1>::smem()};
-    case kStrip32x128: return {32, 128, StripK<32, 128, 1>::fn(), StripK<32, 128, 1>::smem()};
-    default: return {0, 0, nullptr, 0};
+    case kStrip128x16: return {128, 16, 4, StripK<128, 16, 8, 4, 3>::fn(), StripK<128, 16, 8, 4, 3>::smem()};
+    case kStrip128x32: return {128, 32, 2, StripK<128, 32, 8, 2, 5>::fn(), StripK<128, 32, 8, 2, 5>::smem()};
+    case kStrip128x64: return {128, 64, 2, StripK<128, 64, 4, 2, 4>::fn(), StripK<128, 64, 4, 2, 4>::smem()};
+    case kStrip16x128: return {16, 128, 4, StripK<16, 128, 1, 4, 3>::fn(), StripK<16, 128, 1, 4, 3>::smem()};
+    case kStrip32x128: return {32, 128, 2, StripK<32, 128, 1, 2, 5>::fn(), StripK<32, 128, 1, 2, 5>::smem()};
+    default: return {0, 0, 1, nullptr, 0};
   }
 }
 

@@ -145,6 +145,15 @@ int tb_gpu_tiled_multiply_flat_ex(int32_t device, const double* a, const double*
   const bool direct_pageable = !(pin_a || stage_a) || !(pin_b || stage_b) || !(pin_c || stage_c);
   StageRing& ring = g_ring[device];
   if ((stage_a || stage_b || stage_c) && (s = ring.ensure())) return s;
+  struct PoolSession {  // copy workers spin (not sleep) between this call's staging copies
+    CopyPool* pool;
+    explicit PoolSession(CopyPool* p) : pool(p) {
+      if (pool) pool->set_active(true);
+    }
+    ~PoolSession() {
+      if (pool) pool->set_active(false);
+    }
+  } pool_session((stage_a || stage_b || stage_c) ? ring.pool.get() : nullptr);
 
   // Copy/compute/copy pipeline over four streams (H2D, two compute, D2H).
   //  Phase 1 (rank-k panels): the first Mq rows of C are computed as

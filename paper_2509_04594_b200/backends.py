@@ -190,15 +190,15 @@ def gpu_tiled_multiply(a, b, tile: TileConfig = TileConfig(), variant="auto", de
     so it goes through the host-buffer entry: its copy/compute pipeline
     stages the caller's pageable numpy arrays through pinned slots and
     overlaps the copies with the GEMM (N = 10000: 567 ms through plain
-    upload + GEMM + download before). Kernel-only seconds for FLOPS records
+    upload + GEMM + download before, 72 ms now; N = 4000: 85 -> 14 ms). Kernel-only seconds for FLOPS records
     come from ``gpu_tiled_multiply_timed``."""
     a, b = require_operands(a, b)
     tile.validate()
     m, k = a.shape
     n = b.shape[1]
-    if 2.0 * m * n * k < 1e10:
-        # small products: a plain upload / launch / download is quicker than
-        # staging (N = 1000: 1.5 vs 2.2 ms; N = 2000: 7.5 vs 5.3 ms)
+    if 2.0 * m * n * k < 1e9:
+        # tiny products: a plain upload / launch / download costs the same
+        # (N = 500: 0.55 ms either way; N = 1000: 1.57 vs 0.92 ms staged)
         return gpu_tiled_multiply_timed(a, b, tile, variant, device)[0]
     out = np.empty((m, n), dtype=np.float64)
     sec = np.zeros(1)

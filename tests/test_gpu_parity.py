@@ -574,3 +574,29 @@ def test_dimension_limits(tb):
     assert lib.tb_validate_launch(4, 4, 4, 32, 9, 0) == tb.STATUS_BAD_DIMS
     assert lib.tb_validate_launch(4, 4, 4, 32, 0, 0) == tb.STATUS_OK
     assert lib.tb_validate_launch(4, 4, 4, 32, 0, 999) == tb.STATUS_NO_DEVICE
+
+
+def test_performance_floor(tb):
+    """Loose guard against silent slow paths (a wrong loader, a lost
+    schedule, a CPU detour): kernel-only N = 4096 >= 25 TFLOP/s (measured
+    ~35), pinned host-buffer N = 6000 end to end >= 15 TFLOP/s (measured
+    ~23, PCIe-bound at this size)."""
+    import torch
+
+    n = 4096
+    g = torch.Generator(device="cuda").manual_seed(3)
+    a = torch.rand((n, n), dtype=torch.float64, device="cuda", generator=g)
+    b = torch.rand((n, n), dtype=torch.float64, device="cuda", generator=g)
+    c = torch.empty_like(a)
+    best = min(tb.dgemm(a, b, c)[1] for _ in range(4))
+    assert tb.flop_count(n) / best / 1e12 >= 25.0, best
+    n = 6000
+    ah = torch.rand((n, n), dtype=torch.float64).pin_memory()
+    bh = torch.rand((n, n), dtype=torch.float64).pin_memory()
+    ch = torch.empty((n, n), dtype=torch.float64).pin_memory()
+    e2e = np.zeros(1)
+    times = []
+    for _ in range(3):
+        assert tb.gpu_tiled_multiply_flat(0, ah, bh, n, n, n, 32, ch, np.zeros(1), out_e2e_seconds=e2e) == 0
+        times.append(e2e[0])
+    assert tb.flop_count(n) / min(times) / 1e12 >= 15.0, times

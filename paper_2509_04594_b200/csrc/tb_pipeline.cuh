@@ -87,8 +87,22 @@ PipePlan plan_pipeline(int64_t m, int64_t k, int64_t n, int sms, bool fused_ok) 
     gb = (groups >= 2 && Mq >= 2048) ? std::vector<int64_t>{0, (Mq / 2 + 127) / 128 * 128, Mq}
                                      : std::vector<int64_t>{0, Mq};
     int64_t r = m - Mq;
-    std::vector<int64_t> tail;
-    for (int64_t t : {std::min<int64_t>(128, blk / 4), blk / 2})  // shrinking tail: the last D2H is ~10-20 MB
+    std::vector<int64_t> tail, tsz{std::min<int64_t>(128, blk / 4), blk / 6, blk / 3};
+    // TB_TAIL=t0,t1,... (last block first) overrides the tail sizes (tuning).
+    if (const char* e = std::getenv("TB_TAIL")) {
+      tsz.clear();
+      for (const char* q = e; *q;) {
+        char* end = nullptr;
+        const long long v = std::strtoll(q, &end, 10);
+        if (end == q) break;
+        if (v > 0) tsz.push_back(v);
+        q = *end == ',' ? end + 1 : end;
+      }
+    }
+    // Shrinking tail (N = 10000: ..., 512, 256, 144 rows): each block's D2H
+    // ends about when the next block's GEMM does, so the copies after the
+    // last GEMM are ~20 MB (57.4 -> 57.1 ms, profiles/r01_pipe_tail_sweep.txt).
+    for (int64_t t : tsz)
       if (t > 0 && r >= 2 * t) {
         tail.push_back(t);
         r -= t;

@@ -1,7 +1,13 @@
-"""Time the host-buffer pipeline (tb_gpu_tiled_multiply_flat_ex) for several
-TB_PIPE=R,P,Q shapes in subprocesses (tooling)."""
+"""Time the host-buffer pipeline (tb_gpu_tiled_multiply_flat_ex) under
+several environment settings, each in its own subprocess, interleaved over
+rounds (tooling).
+
+    python tools/pipe_tune.py N ROUNDS spec ...
+    spec = default | VAR=value[;VAR=value]      e.g. TB_TAIL=128,384,768
+"""
 import json
 import os
+import statistics
 import subprocess
 import sys
 
@@ -15,22 +21,34 @@ a = (torch.rand((n, n), dtype=torch.float64, generator=g) * 3 + 2).pin_memory()
 b = (torch.rand((n, n), dtype=torch.float64, generator=g) * 3 + 2).pin_memory()
 c = torch.empty((n, n), dtype=torch.float64).pin_memory()
 s, e = np.zeros(1), np.zeros(1)
-best = 1e9
-for i in range(4):
+es, ks = [], []
+for i in range(9):
     assert tb.gpu_tiled_multiply_flat(0, a, b, n, n, n, 32, c, s, out_e2e_seconds=e) == 0
-    if i: best = min(best, e[0])
-print(best, s[0])
+    if i: es.append(e[0]); ks.append(s[0])
+es.sort(); ks.sort()
+print(es[len(es) // 2], es[0], ks[len(ks) // 2])
 '''
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 10000
-shapes = sys.argv[2:] or ["default", "8,8,2", "8,8,3", "8,16,2", "16,8,4", "8,4,2", "4,8,1", "16,16,4"]
-for sh in shapes:
-    env = dict(os.environ)
-    if sh != "default":
-        env["TB_PIPE"] = sh
-    out = subprocess.run([sys.executable, "-c", CODE, str(n)], env=env, capture_output=True, text=True)
-    try:
-        e2e, ks = map(float, out.stdout.split())
-        print(json.dumps({"pipe": sh, "n": n, "e2e_ms": e2e * 1e3, "kernel_ms": ks * 1e3,
-                          "e2e_tflops": (2 * n**3 - n**2) / e2e / 1e12}))
-    except ValueError:
-        print(sh, out.stdout[-300:], out.stderr[-500:])
+rounds = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+specs = sys.argv[3:] or ["default"]
+res = {sp: [] for sp in specs}
+for rd in range(rounds):
+    for sp in specs:
+        env = dict(os.environ)
+        if sp != "default":
+            for kv in sp.split(";"):
+                k, v = kv.split("=", 1)
+                env[k] = v
+        out = subprocess.run([sys.executable, "-c", CODE, str(n)], env=env, capture_output=True, text=True)
+        try:
+            med, best, kmed = map(float, out.stdout.split())
+        except ValueError:
+            print(sp, out.stdout[-300:], out.stderr[-500:], flush=True)
+            continue
+        res[sp].append(med)
+        print(json.dumps({"spec": sp, "round": rd, "n": n, "e2e_ms_median": med * 1e3, "e2e_ms_best": best * 1e3,
+                          "kernel_ms": kmed * 1e3}), flush=True)
+for sp, v in res.items():
+    if v:
+        m = statistics.median(v)
+        print(f"{sp:40s} median-of-rounds {m * 1e3:8.3f} ms  {(2 * n**3 - n**2) / m / 1e12:6.2f} TFLOP/s")

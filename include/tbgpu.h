@@ -107,6 +107,25 @@ TB_API int tb_cublas_dgemm(const double* A, const double* B, double* C, int64_t 
                     int64_t n, int32_t tile_edge, int32_t variant, int32_t device,
                     void* cuda_stream, double* out_kernel_seconds);
 
+/* Row-sharded multi-GPU GEMM from one process (the
+ * reference's multi-device row partition is plan_partitions,
+ * backends.py:119-136). Entry i of `devices` owns rows[i] rows:
+ * C_rows[i] (rows[i] x n) = A_rows[i] (rows[i] x k) · B, all packed
+ * row-major on devices[i]; rows[i] may be 0. B_root (k x n) is on
+ * devices[0]; B_replicas[i] (k x n, i >= 1) receives B on devices[i]
+ * (entry 0 unused; the table may be NULL when ndev == 1). B is forwarded
+ * in K-panels down the chain devices[0] -> devices[1] -> ... by peer copies
+ * overlapped with each device's panel GEMMs. A device may appear more than
+ * once (tests). The caller's buffers must be ready before the call (it does
+ * not order itself after the caller's streams); synchronous.
+ * out_kernel_seconds_max: max over devices of first-GEMM start .. last-GEMM
+ * end (CUDA events); out_total_seconds (nullable): host clock around the
+ * whole exchange + compute. variant: AUTO / DMMA_* / DFMA (not PAPER). */
+TB_API int tb_dgemm_mgpu(int32_t ndev, const int32_t* devices, const double* const* A_rows,
+                         const double* B_root, double* const* B_replicas, double* const* C_rows,
+                         const int64_t* rows, int64_t k, int64_t n, int32_t variant,
+                         double* out_kernel_seconds_max, double* out_total_seconds);
+
 /* Launch validation only (limits.ts:58-79 validateLaunch), no device work
  * beyond attribute queries: returns the status tb_dgemm would return for
  * these arguments before launching. */

@@ -17,7 +17,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libtbgpu.so")
 SOURCES = ["tb_capi.cu"]
-DEPS = ["tb_capi.cu", "tb_state.cuh", "tb_launch.cuh", "tb_pipeline.cuh", "dgemm_dmma.cuh", "dgemm_paper.cuh", "ptx.cuh"]
+DEPS = ["tb_capi.cu", "tb_state.cuh", "tb_launch.cuh", "tb_pipeline.cuh", "tb_staging.cuh", "tb_mgpu.cuh", "dgemm_dmma.cuh", "dgemm_paper.cuh", "ptx.cuh"]
 
 
 def nvcc() -> str:

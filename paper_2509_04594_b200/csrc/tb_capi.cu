@@ -33,6 +33,7 @@
 #include "tb_launch.cuh"
 #include "tb_pipeline.cuh"
 #include "tb_staging.cuh"
+#include "tb_mgpu.cuh"
 
 extern "C" {
 
@@ -512,6 +513,13 @@ int tb_pipeline_plan(int64_t m, int64_t k, int64_t n, int32_t sms, int32_t fused
   std::copy(pl.pk.begin(), pl.pk.end(), out_panels);
   std::copy(pl.rb.begin(), pl.rb.end(), out_blocks);
   return TB_STATUS_OK;
+}
+
+int tb_dgemm_mgpu(int32_t ndev, const int32_t* devices, const double* const* A_rows, const double* B_root,
+                  double* const* B_replicas, double* const* C_rows, const int64_t* rows, int64_t k, int64_t n,
+                  int32_t variant, double* out_kernel_seconds_max, double* out_total_seconds) {
+  return mgpu_run(ndev, devices, A_rows, B_root, B_replicas, C_rows, rows, k, n, variant, out_kernel_seconds_max,
+                  out_total_seconds);
 }
 
 long long tb_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }

@@ -21,7 +21,7 @@ from typing import Callable
 import torch
 import torch.distributed as dist
 
-__all__ = ["row_partitions", "panel_bounds", "ramp_panel_bounds", "gathered_panels", "ShardedGemm", "HostShardedGemm", "gather_rows"]
+__all__ = ["row_partitions", "panel_bounds", "ramp_panel_bounds", "gathered_panels", "ShardedGemm", "HostShardedGemm", "gather_rows", "peer_sharded_dgemm"]
 
 
 def row_partitions(m: int, world: int) -> list[tuple[int, int]]:
@@ -239,3 +239,48 @@ def gather_rows(out_local: torch.Tensor, parts: list[tuple[int, int]], dst: int 
     if rank != dst:
         return None
     return torch.cat([g[: r1 - r0] for g, (r0, r1) in zip(gathered, parts)], dim=0)
+
+
+def peer_sharded_dgemm(a_rows: list, b_root: torch.Tensor, c_rows: list, b_replicas: list | None = None,
+                       variant="auto") -> tuple[float, float]:
+    """Single-process form (``tb_dgemm_mgpu``): ``c_rows[i] = a_rows[i] · B``
+    with every ``a_rows[i]`` / ``c_rows[i]`` (and ``b_replicas[i]``, i >= 1)
+    a contiguous float64 CUDA tensor on device i's GPU and B on the GPU of
+    ``a_rows[0]``. B is forwarded down the device chain in K-panels by peer
+    copies overlapped with the panel GEMMs; ``b_replicas`` defaults to fresh
+    buffers. Returns ``(kernel_seconds_max, total_seconds)``."""
+    import ctypes
+
+    from . import _lib
+    from .errors import ShapeError
+
+    nd = len(a_rows)
+    if nd < 1 or len(c_rows) != nd:
+        raise ShapeError(f"need one C block per A block, got {nd} and {len(c_rows)}")
+    k, n = b_root.shape
+    for i, (a, c) in enumerate(zip(a_rows, c_rows)):
+        for t, name in ((a, "a"), (c, "c")):
+            if t.dtype != torch.float64 or not t.is_cuda or not t.is_contiguous():
+                raise ShapeError(f"{name}_rows[{i}] must be a contiguous float64 CUDA tensor")
+        if a.shape[1] != k or tuple(c.shape) != (a.shape[0], n) or a.device != c.device:
+            raise ShapeError(f"block {i}: {tuple(a.shape)} @ {k}x{n} -> {tuple(c.shape)} on {a.device}/{c.device}")
+    if b_root.dtype != torch.float64 or not b_root.is_cuda or not b_root.is_contiguous() \
+            or b_root.device != a_rows[0].device:
+        raise ShapeError("b_root must be a contiguous float64 CUDA tensor on a_rows[0]'s device")
+    if b_replicas is None:
+        b_replicas = [None] + [torch.empty((k, n), dtype=torch.float64, device=a.device) for a in a_rows[1:]]
+    for i in range(1, nd):
+        r = b_replicas[i]
+        if r is None or tuple(r.shape) != (k, n) or r.device != a_rows[i].device or not r.is_contiguous():
+            raise ShapeError(f"b_replicas[{i}] must be a contiguous {k}x{n} tensor on {a_rows[i].device}")
+    for d in {a.device.index for a in a_rows}:
+        torch.cuda.synchronize(d)  # the call does not order itself after torch's streams
+    devs = (ctypes.c_int32 * nd)(*[a.device.index for a in a_rows])
+    ap = (ctypes.c_void_p * nd)(*[a.data_ptr() for a in a_rows])
+    cp = (ctypes.c_void_p * nd)(*[c.data_ptr() for c in c_rows])
+    bp = (ctypes.c_void_p * nd)(*([0] + [r.data_ptr() for r in b_replicas[1:]]))
+    rows = (ctypes.c_int64 * nd)(*[a.shape[0] for a in a_rows])
+    kmax, total = ctypes.c_double(), ctypes.c_double()
+    _lib.check(_lib.lib().tb_dgemm_mgpu(nd, devs, ap, b_root.data_ptr(), bp, cp, rows, k, n,
+                                        _lib.variant_id(variant), ctypes.byref(kmax), ctypes.byref(total)))
+    return kmax.value, total.value

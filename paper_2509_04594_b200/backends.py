@@ -168,19 +168,58 @@ def _device_index(device) -> int:
     return 0 if device is None else int(device)
 
 
-def gpu_tiled_multiply_timed(a, b, tile: TileConfig = TileConfig(), variant="auto", device=None):
+class _CopyClock:
+    """CUDA-event clock around the upload and the download of a timed call
+    (transfers measured separately, reported as metadata)."""
+
+    def __init__(self, torch, dev, transfers):
+        self.torch, self.dev, self.tr = torch, dev, transfers
+        self.ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)] if transfers is not None else None
+
+    def mark(self, i):
+        if self.ev is not None:
+            self.ev[i].record(self.torch.cuda.current_stream(self.dev))
+
+    def finish(self, h2d_bytes, d2h_bytes):
+        if self.ev is None:
+            return
+        self.ev[3].synchronize()
+        self.tr.update(h2d_seconds=self.ev[0].elapsed_time(self.ev[1]) * 1e-3,
+                       d2h_seconds=self.ev[2].elapsed_time(self.ev[3]) * 1e-3,
+                       h2d_bytes=h2d_bytes, d2h_bytes=d2h_bytes)
+
+
+def gpu_tiled_multiply_timed(a, b, tile: TileConfig = TileConfig(), variant="auto", device=None, transfers=None):
     """``(product, kernel_seconds)``: upload, sm_100a kernel, download.
 
     Uploads/downloads sit outside the kernel clock, exactly as the reference
-    device copies operands before its clock starts (executor.ts:92-104)."""
+    device copies operands before its clock starts (executor.ts:92-104).
+    A ``transfers`` dict, if given, receives the copies' own event-timed
+    seconds and bytes (``h2d_seconds``, ``d2h_seconds``, ``h2d_bytes``,
+    ``d2h_bytes``)."""
     torch = _torch()
     a, b = require_operands(a, b)
     tile.validate()
     dev = torch.device("cuda", _device_index(device))
+    clk = _CopyClock(torch, dev, transfers)
+    clk.mark(0)
     ta = torch.from_numpy(a).to(dev)
     tb = torch.from_numpy(b).to(dev)
+    clk.mark(1)
     out, sec = dgemm(ta, tb, tile_edge=tile.k, variant=variant)
-    return out.cpu().numpy(), sec
+    clk.mark(2)
+    host = out.cpu().numpy()
+    clk.mark(3)
+    clk.finish(a.nbytes + b.nbytes, host.nbytes)
+    return host, sec
+
+
+def _with_transfers(timed, *args):
+    """Registry form of a timed backend: ``(product, kernel_seconds,
+    transfers)``; the runner aggregates the third element into metadata."""
+    tr = {}
+    out, sec = timed(*args, transfers=tr)
+    return out, sec, tr
 
 
 def gpu_tiled_multiply(a, b, tile: TileConfig = TileConfig(), variant="auto", device=None) -> np.ndarray:
@@ -206,12 +245,20 @@ def gpu_tiled_multiply(a, b, tile: TileConfig = TileConfig(), variant="auto", de
     return out
 
 
-def cublas_multiply_timed(a, b, device=None):
+def cublas_multiply_timed(a, b, device=None, transfers=None):
     torch = _torch()
     a, b = require_operands(a, b)
     dev = torch.device("cuda", _device_index(device))
-    out, sec = cublas_dgemm(torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev))
-    return out.cpu().numpy(), sec
+    clk = _CopyClock(torch, dev, transfers)
+    clk.mark(0)
+    ta, tb = torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev)
+    clk.mark(1)
+    out, sec = cublas_dgemm(ta, tb)
+    clk.mark(2)
+    host = out.cpu().numpy()
+    clk.mark(3)
+    clk.finish(a.nbytes + b.nbytes, host.nbytes)
+    return host, sec
 
 
 def cublas_multiply(a, b, device=None) -> np.ndarray:
@@ -331,17 +378,17 @@ def register_gpu_backend(registry: BackendRegistry | None = None, device=None, v
     desc = registry._register(
         BackendDescriptor(GPU_BACKEND_NAME, parallel=True, requires_external=True),
         lambda tile, pool: (lambda a, b: gpu_tiled_multiply(a, b, tile, variant, device)),
-        lambda tile, pool: (lambda a, b: gpu_tiled_multiply_timed(a, b, tile, variant, device)),
+        lambda tile, pool: (lambda a, b: _with_transfers(gpu_tiled_multiply_timed, a, b, tile, variant, device)),
     )
     registry._register(
         BackendDescriptor(PAPER_BACKEND_NAME, parallel=True, requires_external=True),
         lambda tile, pool: (lambda a, b: gpu_tiled_multiply(a, b, tile, "paper", device)),
-        lambda tile, pool: (lambda a, b: gpu_tiled_multiply_timed(a, b, tile, "paper", device)),
+        lambda tile, pool: (lambda a, b: _with_transfers(gpu_tiled_multiply_timed, a, b, tile, "paper", device)),
     )
     registry._register(
         BackendDescriptor(CUBLAS_BACKEND_NAME, parallel=True, requires_external=True),
         lambda tile, pool: (lambda a, b: cublas_multiply(a, b, device)),
-        lambda tile, pool: (lambda a, b: cublas_multiply_timed(a, b, device)),
+        lambda tile, pool: (lambda a, b: _with_transfers(cublas_multiply_timed, a, b, device)),
     )
     return desc
 

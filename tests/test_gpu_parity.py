@@ -228,6 +228,15 @@ def test_registry_and_device_timed_runner(tb, oracle, tmp_path):
     tb.write_records(path, records, meta)
     lines = path.read_text().splitlines()
     assert lines[0] == "backend,n,trial,seconds,flops" and len(lines) == 13
+    # host<->device copies timed separately, reported as metadata
+    import json
+
+    tr = json.loads((tmp_path / "gpu.csv.meta.json").read_text())["config"]["transfers"]
+    for name in (tb.GPU_BACKEND_NAME, tb.CUBLAS_BACKEND_NAME):
+        cell = tr[name]["129"]
+        assert cell["trials"] == 3
+        assert cell["h2d_bytes"] == 2 * 8 * 129 * 129 and cell["d2h_bytes"] == 8 * 129 * 129
+        assert cell["h2d_seconds_median"] > 0 and cell["d2h_seconds_median"] > 0
 
 
 def test_liar_backend_caught_by_verify(tb, oracle):

@@ -37,12 +37,12 @@ def _sanitizer():
 
 
 def test_driver_plain(driver):
-    res = subprocess.run([driver, "--pipeline"], capture_output=True, text=True, timeout=300)
+    res = subprocess.run([driver, "--pipeline", "--mgpu"], capture_output=True, text=True, timeout=300)
     assert res.returncode == 0, res.stdout + res.stderr
 
 
 @pytest.mark.parametrize("bm", ["", "128"])
-@pytest.mark.parametrize("tool,args", [("memcheck", ["--pipeline"]), ("synccheck", []), ("racecheck", ["--tma-only"])])
+@pytest.mark.parametrize("tool,args", [("memcheck", ["--pipeline", "--mgpu"]), ("synccheck", ["--mgpu"]), ("racecheck", ["--tma-only"])])
 def test_sanitizer_clean(driver, tool, args, bm):
     """racecheck runs on the TMA-fed variants and the paper kernel only: it
     tracks 8-byte cp.async shared writes but not the mbarrier arrive/wait that

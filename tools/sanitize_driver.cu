@@ -14,17 +14,20 @@
 
 #include "tbgpu.h"
 
-// Usage: sanitize_driver [--tma-only] [--pipeline]
+// Usage: sanitize_driver [--tma-only] [--pipeline] [--mgpu]
 //   --tma-only: even shapes and TMA-fed variants only (racecheck does not
 //   model mbarrier-ordered cp.async writes; see tests/test_gpu_sanitizer.py).
 //   --pipeline: also one host-buffer call large enough for the copy/compute
 //   pipeline (the flag-driven PIPE-mode phase-1 launch + row blocks).
+//   --mgpu: also tb_dgemm_mgpu with device 0 listed three times (chain of
+//   peer copies + K-panel GEMMs, a zero-row entry, 64-row panels).
 // TB_BM=128 in the environment forces the 128-row tiles on these small shapes.
 int main(int argc, char** argv) {
-  bool tma_only = false, pipeline = false;
+  bool tma_only = false, pipeline = false, mgpu = false;
   for (int i = 1; i < argc; ++i) {
     tma_only |= std::string(argv[i]) == "--tma-only";
     pipeline |= std::string(argv[i]) == "--pipeline";
+    mgpu |= std::string(argv[i]) == "--mgpu";
   }
   struct Shape {
     long m, k, n;
@@ -87,6 +90,55 @@ int main(int argc, char** argv) {
     const bool ok = st == TB_STATUS_OK && rel <= 1e-12;
     failures += !ok;
     std::printf("pipeline %ldx%ldx%ld status=%d normwise=%.2e %s\n", m, k, n, st, rel, ok ? "ok" : tb_last_error());
+  }
+  if (mgpu) {
+    const long k = 300, n = 258;
+    const long rows[3] = {70, 0, 133};
+    std::vector<double> b(k * n);
+    for (size_t i = 0; i < b.size(); ++i) b[i] = 2.0 + 3.0 * ((i * 40503u) % 1000) / 1000.0;
+    double *dB, *dA[3] = {}, *dC[3] = {}, *dR[3] = {};
+    cudaMalloc(&dB, b.size() * 8);
+    cudaMemcpy(dB, b.data(), b.size() * 8, cudaMemcpyHostToDevice);
+    std::vector<std::vector<double>> a(3);
+    for (int d = 0; d < 3; ++d) {
+      a[d].resize(rows[d] * k);
+      for (size_t i = 0; i < a[d].size(); ++i) a[d][i] = 2.0 + 3.0 * (((i + 977 * d) * 2654435761u) % 1000) / 1000.0;
+      if (rows[d]) {
+        cudaMalloc(&dA[d], a[d].size() * 8);
+        cudaMalloc(&dC[d], rows[d] * n * 8);
+        cudaMemcpy(dA[d], a[d].data(), a[d].size() * 8, cudaMemcpyHostToDevice);
+      }
+      if (d) cudaMalloc(&dR[d], b.size() * 8);
+    }
+    setenv("TB_MGPU_PANEL", "64", 1);
+    const int devs[3] = {0, 0, 0};
+    const int64_t rws[3] = {rows[0], rows[1], rows[2]};
+    double kmax = 0, total = 0;
+    const int st = tb_dgemm_mgpu(3, devs, dA, dB, dR, dC, rws, k, n, TB_VARIANT_AUTO, &kmax, &total);
+    unsetenv("TB_MGPU_PANEL");
+    double num = 0, den = 0;
+    for (int d = 0; d < 3; ++d) {
+      if (!rows[d]) continue;
+      std::vector<double> c(rows[d] * n);
+      cudaMemcpy(c.data(), dC[d], c.size() * 8, cudaMemcpyDeviceToHost);
+      for (long i = 0; i < rows[d]; ++i)
+        for (long j = 0; j < n; ++j) {
+          double r = 0;
+          for (long p = 0; p < k; ++p) r += a[d][i * k + p] * b[p * n + j];
+          num += (c[i * n + j] - r) * (c[i * n + j] - r);
+          den += r * r;
+        }
+    }
+    const double rel = std::sqrt(num / den);
+    const bool ok = st == TB_STATUS_OK && rel <= 1e-12;
+    failures += !ok;
+    std::printf("mgpu 3 entries k=%ld n=%ld status=%d normwise=%.2e %s\n", k, n, st, rel, ok ? "ok" : tb_last_error());
+    for (int d = 0; d < 3; ++d) {
+      cudaFree(dA[d]);
+      cudaFree(dC[d]);
+      cudaFree(dR[d]);
+    }
+    cudaFree(dB);
   }
   tb_release();
   return failures ? 1 : 0;

@@ -239,7 +239,7 @@ def run_ours(args) -> None:
         b.copy_(torch.rand((n, n), dtype=torch.float64, device=dev, generator=g) * 3.0 + 2.0)
     c_loc = torch.empty((r1 - r0, n), dtype=torch.float64, device=dev)
     stream = torch.cuda.current_stream()
-    sharded = ShardedGemm(panels=args.panels) if world > 1 else None
+    sharded = ShardedGemm(panels=args.panels or None) if world > 1 else None
 
     def step():
         if world > 1:
@@ -333,7 +333,7 @@ def run_ours(args) -> None:
     out_s = np.zeros(1)
     e2e = np.zeros(1)
     e2e_times, e2e_dev = [], []
-    host_sharded = HostShardedGemm(panels=args.panels) if world > 1 else None
+    host_sharded = HostShardedGemm(panels=args.panels or 4) if world > 1 else None
     for i in range(1 + max(2, args.steps // 3)):
         if world > 1:
             dist.barrier()
@@ -377,8 +377,8 @@ def run_ours(args) -> None:
             "config": {"workload": f"N={n} FP64 square GEMM C=A*B (BASELINE configs[3], 1..8 GPUs)", "n": n,
                        "tile": "128x128x16 CTA, 8 DMMA warps + TMA producer warpgroup, 6 stages",
                        "variant": args.variant, "parallelism": f"row-shard{world}" + (
-                           f" + NCCL broadcast of B ({args.panels} K-panels)" if world > 1 else ""),
-                       "l2": "inputs (800 MB/matrix) larger than L2; no flush"},
+                           f" + NCCL broadcast of B ({args.panels or 'geometric'} K-panels)" if world > 1 else ""),
+                       "l2": f"inputs ({8 * n * n / 1e6:.0f} MB/matrix) larger than L2 (126 MB); no flush"},
             "pct_fp64_peak": 100.0 * value / 1e3 / peak,
             "pct_fp64_peak_40tf": 100.0 * value / 1e3 / 40.0,
             "cublas_gflops": cublas_gflops,
@@ -419,7 +419,8 @@ def main():
     p.add_argument("--size", dest="n", type=int, default=10000, help="matrix order N")
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--variant", default="auto")
-    p.add_argument("--panels", type=int, default=4, help="K-panels of the B broadcast at N>1")
+    p.add_argument("--panels", type=int, default=0,
+                   help="K-panels of the B broadcast at N>1 (0: geometric 128, x3, ... for the device path, 4 for the host path)")
     p.add_argument("--ref-seconds", type=float, default=10.0, help="CPU sample length per measurement (s)")
     p.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     p.add_argument("--dist-backend", default="nccl", help="torch.distributed backend at N>1 (nccl; gloo for tests)")

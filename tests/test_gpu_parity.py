@@ -267,7 +267,7 @@ def test_sharded_gemm_single_rank_nccl_panels(tb, oracle):
         ta = torch.from_numpy(a[r0:r1]).cuda()
         tb_ = torch.from_numpy(b).cuda()
         ref = oracle.tiled_parallel(a, b)
-        for panels in (1, 4, 7):
+        for panels in (None, 1, 4, 7):
             out = torch.empty((r1 - r0, n), dtype=torch.float64, device="cuda")
             ShardedGemm(panels=panels)(ta, tb_, out)
             torch.cuda.synchronize()

@@ -52,7 +52,7 @@ def _worker(rank, world, port, n, panels, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("n,panels", [(37, 1), (64, 3), (5, 2)])
+@pytest.mark.parametrize("n,panels", [(37, 1), (64, 3), (5, 2), (700, None)])
 def test_sharded_world2(n, panels):
     ctx = mp.get_context("spawn")
     q = ctx.SimpleQueue()
@@ -142,3 +142,16 @@ def test_ramp_panel_bounds():
             assert all(k1 > k0 and k0 % 2 == 0 for k0, k1 in b)
             if len(b) > 2 and k >= 1000:
                 assert b[0][1] - b[0][0] <= (b[1][1] - b[1][0]) // 4  # short first panel
+
+
+def test_geometric_panel_bounds():
+    from paper_2509_04594_b200.multigpu import geometric_panel_bounds
+
+    assert geometric_panel_bounds(10000) == [(0, 128), (128, 512), (512, 1664), (1664, 5120), (5120, 10000)]
+    for k in (1, 2, 3, 5, 37, 127, 128, 129, 1000, 10000, 32768):
+        b = geometric_panel_bounds(k)
+        assert b[0][0] == 0 and b[-1][1] == k
+        assert all(x1 == y0 for (_, x1), (y0, _) in zip(b, b[1:]))
+        assert all(k1 > k0 for k0, k1 in b)
+        assert all(k0 % 2 == 0 for k0, _ in b)          # TMA alignment of every panel start
+        assert len(b) <= 8

@@ -126,6 +126,14 @@ TB_API int tb_dgemm_mgpu(int32_t ndev, const int32_t* devices, const double* con
                          const int64_t* rows, int64_t k, int64_t n, int32_t variant,
                          double* out_kernel_seconds_max, double* out_total_seconds);
 
+/* Asynchronous 2D copy (cudaMemcpy2DAsync, direction inferred from the
+ * pointers): `rows` rows of `width_bytes` from src (pitch spitch_bytes) to dst
+ * (pitch dpitch_bytes) on `cuda_stream`. Plumbing for the host-buffer
+ * multi-GPU driver (multigpu.HostShardedGemm uploads A[:, k-panel] slices
+ * from pinned memory without a host-side gather); no reference counterpart. */
+TB_API int tb_copy2d_async(void* dst, int64_t dpitch_bytes, const void* src, int64_t spitch_bytes,
+                           int64_t width_bytes, int64_t rows, void* cuda_stream);
+
 /* Launch validation only (limits.ts:58-79 validateLaunch), no device work
  * beyond attribute queries: returns the status tb_dgemm would return for
  * these arguments before launching. */

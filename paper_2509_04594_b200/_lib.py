@@ -42,7 +42,7 @@ EXPORTS = [
     "tb_gpu_tiled_multiply_flat", "tb_gpu_tiled_multiply_flat_ex", "tb_dgemm", "tb_dgemm_launch",
     "tb_cublas_dgemm", "tb_validate_launch", "tb_device_count", "tb_variant_name",
     "tb_resolve_variant", "tb_last_error", "tb_version", "tb_release", "tb_pipeline_plan",
-    "tb_kernel_launches", "tb_dgemm_mgpu",
+    "tb_kernel_launches", "tb_dgemm_mgpu", "tb_copy2d_async",
 ]
 
 _D = ctypes.POINTER(ctypes.c_double)
@@ -85,7 +85,8 @@ def _declare(l):
     l.tb_kernel_launches.restype = ctypes.c_longlong
     l.tb_pipeline_plan.argtypes = [_I64, _I64, _I64, _I32, _I32, _P64, _P32, _P64, _I32, _P32, _P64, _I32, _P32]
     l.tb_dgemm_mgpu.argtypes = [_I32, _P32, _VP, _VP, _VP, _VP, _P64, _I64, _I64, _I32, _D, _D]
-    for name in ("tb_dgemm_mgpu", "tb_gpu_tiled_multiply_flat", "tb_gpu_tiled_multiply_flat_ex", "tb_dgemm", "tb_cublas_dgemm",
+    l.tb_copy2d_async.argtypes = [_VP, _I64, _VP, _I64, _I64, _I64, _VP]
+    for name in ("tb_copy2d_async", "tb_dgemm_mgpu", "tb_gpu_tiled_multiply_flat", "tb_gpu_tiled_multiply_flat_ex", "tb_dgemm", "tb_cublas_dgemm",
                  "tb_dgemm_launch", "tb_validate_launch", "tb_device_count", "tb_resolve_variant",
                  "tb_pipeline_plan"):
         getattr(l, name).restype = ctypes.c_int

@@ -522,6 +522,19 @@ int tb_dgemm_mgpu(int32_t ndev, const int32_t* devices, const double* const* A_r
                   out_total_seconds);
 }
 
+int tb_copy2d_async(void* dst, int64_t dpitch_bytes, const void* src, int64_t spitch_bytes, int64_t width_bytes,
+                    int64_t rows, void* cuda_stream) {
+  if (!dst || !src || width_bytes < 0 || rows < 0 || dpitch_bytes < width_bytes || spitch_bytes < width_bytes) {
+    set_err("bad 2D copy arguments");
+    return TB_STATUS_BAD_DIMS;
+  }
+  if (width_bytes == 0 || rows == 0) return TB_STATUS_OK;
+  TB_CUDA(cudaMemcpy2DAsync(dst, (size_t)dpitch_bytes, src, (size_t)spitch_bytes, (size_t)width_bytes, (size_t)rows,
+                            cudaMemcpyDefault, static_cast<cudaStream_t>(cuda_stream)),
+          "2D copy");
+  return TB_STATUS_OK;
+}
+
 long long tb_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
 
 void tb_release(void) {

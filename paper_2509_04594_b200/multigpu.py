@@ -21,7 +21,7 @@ from typing import Callable
 import torch
 import torch.distributed as dist
 
-__all__ = ["row_partitions", "panel_bounds", "ramp_panel_bounds", "geometric_panel_bounds", "gathered_panels", "ShardedGemm", "HostShardedGemm", "gather_rows", "peer_sharded_dgemm"]
+__all__ = ["row_partitions", "panel_bounds", "ramp_panel_bounds", "geometric_panel_bounds", "host_panel_bounds", "shrinking_chunks", "gathered_panels", "ShardedGemm", "HostShardedGemm", "gather_rows", "peer_sharded_dgemm"]
 
 
 def row_partitions(m: int, world: int) -> list[tuple[int, int]]:
@@ -105,6 +105,53 @@ def gathered_panels(k: int, world: int, panels: int) -> list[tuple[int, int]]:
     return out
 
 
+def host_panel_bounds(k: int, world: int, first: int = 128, growth: float = 1.6,
+                      last_min: int = 3328) -> list[tuple[int, int]]:
+    """K-panels for ``HostShardedGemm`` (default plan). Every bound is a
+    multiple of 2*world (equal, even per-rank shares; the last panel padded
+    past k like ``gathered_panels``).
+
+    * A ramp from ``first`` rows growing by ``growth``: per k-row a rank
+      uploads 8*m_local + 8n/world bytes over PCIe (N = 10000, 8 GPUs:
+      20 KB, 0.36 us at 55 GB/s, plus the 80 KB gather over NVLink) and
+      multiplies for 2*m_local*n / 35 TF/s = 0.71 us, so each panel may be
+      ~1.6x its predecessor and still land while the previous one computes.
+    * One last panel of at least ``last_min`` rows, split into row chunks
+      whose D2H copies run while later chunks compute: hiding the whole C
+      shard's D2H (8*m_local*n bytes) under the last panel needs
+      2*kl/F >= 8/H_d2h, i.e. kl >= 4F/H = 4 * 35e12 / 55e9 ~ 2550 (x1.3).
+    """
+    unit = 2 * world
+    kp = -(-k // unit) * unit
+    out, k0 = [], 0
+    step = -(-max(first, 1) // unit) * unit
+    while k0 < kp:
+        if kp - k0 <= max(last_min, step + step // 2):
+            out.append((k0, kp))
+            break
+        k1 = min(k0 + step, kp - last_min)
+        k1 = max(k0 + unit, k1 // unit * unit)
+        out.append((k0, k1))
+        k0 = k1
+        step = -(-int(step * growth) // unit) * unit
+    return out
+
+
+def shrinking_chunks(m: int, align: int = 128, last: int = 128) -> list[tuple[int, int]]:
+    """Row chunks for the last panel: each half of what remains (on
+    ``align``-row bounds) until at most ``last`` rows are left, so the D2H
+    after the final chunk is small (N = 10000, 1250 rows: 640, 384, 128, 98)."""
+    out, r0 = [], 0
+    while m - r0 > last:
+        step = -(-((m - r0) // 2) // align) * align
+        step = min(step, m - r0)
+        out.append((r0, r0 + step))
+        r0 += step
+    if r0 < m:
+        out.append((r0, m))
+    return out
+
+
 def _gpu_matmul(a, b, out, accumulate: bool) -> None:
     from .backends import dgemm_launch
     dgemm_launch(a, b, out, accumulate=accumulate)
@@ -158,10 +205,17 @@ class HostShardedGemm:
     panel's GEMM ``C_local (+)= A_local[:, q] · B[q, :]`` runs as soon as its
     gather completes. The last panel's GEMM is split into row chunks whose
     D2H copies overlap the remaining chunks. Device buffers are cached across
-    calls. With ``device='cpu'`` (gloo tests) copies are plain copies."""
+    calls. With ``device='cpu'`` (gloo tests) copies are plain copies.
 
-    def __init__(self, group=None, panels: int = 4, chunks: int = 4, local_matmul: Callable | None = None,
-                 device=None):
+    Default plan (``panels=None``, ``chunks=None``): ``host_panel_bounds``
+    (a ramp of small panels, then one deep last panel) and
+    ``shrinking_chunks``; A is uploaded panel by panel (A[:, q] as a 2D copy
+    from the pinned rows), so the first GEMM waits for ~1 MB of A and one
+    small B share rather than the whole A shard. Integers give the even
+    ``gathered_panels`` split and even chunks."""
+
+    def __init__(self, group=None, panels: int | None = None, chunks: int | None = None,
+                 local_matmul: Callable | None = None, device=None):
         self.group = group
         self.panels = panels
         self.chunks = chunks
@@ -187,7 +241,7 @@ class HostShardedGemm:
         n = b_h.shape[1]
         if b_h.shape[0] != k or tuple(c_local_h.shape) != (m, n):
             raise ValueError(f"shapes {tuple(a_local_h.shape)} @ {tuple(b_h.shape)} -> {tuple(c_local_h.shape)}")
-        bounds = gathered_panels(k, world, self.panels)
+        bounds = host_panel_bounds(k, world) if not self.panels else gathered_panels(k, world, self.panels)
         kp = bounds[-1][1]
         shares = [(k1 - k0) // world for k0, k1 in bounds]
         a_d, b_d, c_d, stage = self._buffers(m, k, kp, n, sum(shares))
@@ -211,13 +265,17 @@ class HostShardedGemm:
                 s0, s1 = k0 + rank * sh, min(k0 + (rank + 1) * sh, k)
                 if s1 > s0:
                     stage[off:off + s1 - s0].copy_(b_h[s0:s1], non_blocking=cuda)
-                if q == 0:
-                    a_d.copy_(a_local_h, non_blocking=cuda)
+                kk1 = min(k1, k)
+                if m > 0 and kk1 > k0:
+                    _copy_cols(a_d, a_local_h, k0, kk1, copy_s)
                 works.append(dist.all_gather_into_tensor(b_d[k0:k1], stage[off:off + sh], group=self.group,
                                                          async_op=True))
                 off += sh
-        step = -(-max(m, 1) // self.chunks)
-        step = -(-step // 128) * 128
+        if self.chunks:
+            step = -(-(-(-max(m, 1) // self.chunks)) // 128) * 128
+            chunks = [(r0, min(m, r0 + step)) for r0 in range(0, m, step)]
+        else:
+            chunks = shrinking_chunks(m)
         for q, (k0, k1) in enumerate(bounds):
             works[q].wait()  # the compute stream (not the host) waits for the gather
             kk1 = min(k1, k)
@@ -227,8 +285,7 @@ class HostShardedGemm:
                 self.local_matmul(a_d[:, k0:kk1], b_d[k0:kk1], c_d, q > 0)
                 continue
             # last panel: row chunks, each copied back as soon as it is final
-            for r0 in range(0, m, step):
-                r1 = min(m, r0 + step)
+            for r0, r1 in chunks:
                 self.local_matmul(a_d[r0:r1, k0:kk1], b_d[k0:kk1], c_d[r0:r1], q > 0)
                 if cuda:
                     back_s.wait_stream(comp)
@@ -238,6 +295,20 @@ class HostShardedGemm:
             back_s.synchronize()  # synchronous call: C is in host memory on return
             comp.wait_stream(back_s)
         return c_local_h
+
+
+def _copy_cols(dst: torch.Tensor, src: torch.Tensor, k0: int, k1: int, stream) -> None:
+    """dst[:, k0:k1] = src[:, k0:k1] between host and device without a
+    host-side gather: one cudaMemcpy2DAsync on ``stream`` (CUDA), or a plain
+    slice copy (CPU tensors, the gloo tests)."""
+    if stream is None:
+        dst[:, k0:k1].copy_(src[:, k0:k1])
+        return
+    from . import _lib
+
+    es = dst.element_size()
+    _lib.check(_lib.lib().tb_copy2d_async(dst.data_ptr() + k0 * es, dst.stride(0) * es, src.data_ptr() + k0 * es,
+                                          src.stride(0) * es, (k1 - k0) * es, dst.shape[0], stream.cuda_stream))
 
 
 class _null:

@@ -281,6 +281,16 @@ def test_sharded_gemm_single_rank_nccl_panels(tb, oracle):
             for _ in range(2):
                 g(a_h, b_h, c_h)
             assert oracle.normwise_rel(c_h.numpy(), ref) <= NORMWISE
+        # default plan on a deeper product: panel ramp + deep last panel, A
+        # uploaded per panel by 2D copies (odd k: the padded last panel)
+        m2, k2, n2 = 700, 5001, 300
+        a2, b2 = oracle.generate(m2, k2, 5), oracle.generate(k2, n2, 6)
+        ref2 = oracle.tiled_parallel(a2, b2)
+        c2 = torch.full((m2, n2), float("nan"), dtype=torch.float64).pin_memory()
+        g = HostShardedGemm()
+        for _ in range(2):
+            g(torch.from_numpy(a2).pin_memory(), torch.from_numpy(b2).pin_memory(), c2)
+        assert oracle.normwise_rel(c2.numpy(), ref2) <= NORMWISE
     finally:
         dist.destroy_process_group()
 

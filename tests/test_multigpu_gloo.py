@@ -108,7 +108,8 @@ def _host_worker(rank, world, port, m, k, n, panels, chunks, q):
 
 
 @pytest.mark.parametrize("m,k,n,panels,chunks", [(37, 41, 29, 3, 2), (64, 64, 64, 1, 4), (5, 3, 7, 2, 1),
-                                                 (300, 200, 100, 4, 3)])
+                                                 (300, 200, 100, 4, 3), (300, 700, 90, None, None),
+                                                 (7, 1001, 33, None, None)])
 def test_host_sharded_world2(m, k, n, panels, chunks):
     """End-to-end multi-GPU form: B uploaded in equal per-rank shares per
     K-panel and rebuilt by all-gather, last panel in row chunks copied back."""
@@ -155,3 +156,24 @@ def test_geometric_panel_bounds():
         assert all(k1 > k0 for k0, k1 in b)
         assert all(k0 % 2 == 0 for k0, _ in b)          # TMA alignment of every panel start
         assert len(b) <= 8
+
+
+def test_host_panel_bounds_and_chunks():
+    from paper_2509_04594_b200.multigpu import host_panel_bounds, shrinking_chunks
+
+    for world in (1, 2, 3, 4, 8):
+        for k in (1, 2, 3, 5, 37, 1000, 4000, 10000, 32768):
+            b = host_panel_bounds(k, world)
+            assert b[0][0] == 0 and b[-1][1] >= k and b[-1][1] - k < 2 * world
+            assert all(x1 == y0 for (_, x1), (y0, _) in zip(b, b[1:]))
+            assert all((k1 - k0) % (2 * world) == 0 and k1 > k0 for k0, k1 in b)
+            if len(b) > 1:
+                assert b[-1][1] - b[-1][0] >= 3328 - 2 * world     # deep last panel hides C's D2H
+    assert [y - x for x, y in host_panel_bounds(10000, 8)] == [128, 208, 336, 544, 880, 1408, 2256, 4240]
+    for m in (0, 1, 127, 128, 129, 1250, 5000, 16384):
+        c = shrinking_chunks(m)
+        assert sum(r1 - r0 for r0, r1 in c) == m
+        assert all(x1 == y0 for (_, x1), (y0, _) in zip(c, c[1:]))
+        assert all(r0 % 128 == 0 for r0, _ in c)
+        if c:
+            assert c[-1][1] - c[-1][0] <= 128

@@ -248,6 +248,16 @@ __global__ void __launch_bounds__(DmmaCfg::THREADS, 1)
             const unsigned long long t_start = globaltimer_ns();
             while (ld_acquire_gpu(&pipe_flags(p)[ready_upto]) == 0)
               if (globaltimer_ns() - t_start > 10000000000ull) __trap();
+            // tooling build: [grid][8] stamps, then [grid][4] producer flag waits
+            // (total ns, count, panel-0 ns, last wait end)
+            TB_TL(if (p.timeline) {
+              unsigned long long* w = p.timeline + 8 * gridDim.x + 4 * blockIdx.x;
+              const unsigned long long t_end = globaltimer_ns();
+              w[0] += t_end - t_start;
+              w[1] += 1;
+              if (ready_upto == 0) w[2] = t_end - t_start;
+              w[3] = t_end;
+            })
           }
           ++ready_upto;
         }

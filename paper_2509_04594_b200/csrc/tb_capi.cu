@@ -451,6 +451,9 @@ int tb_gpu_tiled_multiply_flat_ex(int32_t device, const double* a, const double*
   }
   for (cudaStream_t cs : css) TB_CUDA(cudaStreamSynchronize(cs), "kernel execution");
   const auto h_sync = std::chrono::steady_clock::now();
+#ifdef TB_TIMELINE
+  pipe_timeline_report();
+#endif
   // Kernel-only seconds (outSeconds): the union of the GEMM launches'
   // intervals — launches on the two compute streams overlap, so their sum
   // would count shared time twice.

@@ -354,6 +354,49 @@ int launch_tiles(int dev, const double* A, int64_t lda, const double* B, int64_t
 // A·B over all k, k-panel q (k-stages [panel_it[q], panel_it[q+1]), panel_it
 // in device memory) consumed once flags[q] != 0. TMA operands (even pitch,
 // 16-byte aligned) only.
+#ifdef TB_TIMELINE
+struct PipeTimeline {
+  unsigned long long* buf = nullptr;
+  int grid = 0;
+};
+PipeTimeline g_pipe_tl;  // tooling build: the last PIPE launch's stamps
+
+// Summarise and free the last PIPE launch's stamps (after it completed).
+void pipe_timeline_report() {
+  if (!g_pipe_tl.buf) return;
+  const int g = g_pipe_tl.grid;
+  std::vector<unsigned long long> h((size_t)g * 12);
+  if (cudaMemcpy(h.data(), g_pipe_tl.buf, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost) ==
+      cudaSuccess) {
+    unsigned long long t0 = ~0ull, tend = 0;
+    double wait = 0, wmax = 0, w0 = 0, nw = 0, ml = 0, epi = 0, units = 0, endmin = 1e30, lastw = 0;
+    for (int c = 0; c < g; ++c) t0 = std::min(t0, h[(size_t)c * 8]);
+    for (int c = 0; c < g; ++c) {
+      const unsigned long long* r = &h[(size_t)c * 8];
+      const unsigned long long* w = &h[(size_t)g * 8 + (size_t)c * 4];
+      tend = std::max(tend, r[3]);
+      endmin = std::min(endmin, (double)(r[3] - t0));
+      wait += (double)w[0];
+      wmax = std::max(wmax, (double)w[0]);
+      w0 += (double)w[2];
+      nw += (double)w[1];
+      lastw = std::max(lastw, w[3] ? (double)(w[3] - t0) : 0.0);
+      ml += (double)r[7];
+      epi += (double)r[6];
+      units += (double)r[4];
+    }
+    std::fprintf(stderr,
+                 "TBPIPE grid=%d span_us=%.1f end_min_us=%.1f flag_wait_mean_us=%.1f flag_wait_max_us=%.1f "
+                 "panel0_wait_mean_us=%.1f waits_per_cta=%.2f last_wait_end_us=%.1f mainloop_mean_us=%.1f "
+                 "epilogue_mean_us=%.1f units=%.2f\n",
+                 g, (double)(tend - t0) * 1e-3, endmin * 1e-3, wait / g * 1e-3, wmax * 1e-3, w0 / g * 1e-3, nw / g,
+                 lastw * 1e-3, ml / g * 1e-3, epi / g * 1e-3, units / g);
+  }
+  cudaFree(g_pipe_tl.buf);
+  g_pipe_tl.buf = nullptr;
+}
+#endif
+
 int launch_pipe(int dev, const double* A, int64_t lda, const double* B, int64_t ldb, double* Cm, int64_t ldc,
                 int64_t m, int64_t k, int64_t n, const int* panel_it_d, const int* flags_d, int Q,
                 cudaStream_t stream) {
@@ -389,6 +432,16 @@ int launch_pipe(int dev, const double* A, int64_t lda, const double* B, int64_t 
   if ((s = encode_map(&mB, B, k, n, ldb, Cfg::BK))) return s;
   void* args[] = {&mA, &mB, &p};
   const int grid = (int)std::min<int64_t>(tiles, g_dev[dev].sms);
+#ifdef TB_TIMELINE
+  p.timeline = nullptr;
+  if (std::getenv("TB_TIMELINE")) {  // read back by the host-buffer entry after the call
+    const size_t words = (size_t)grid * 12;
+    TB_CUDA(cudaMalloc(&g_pipe_tl.buf, words * sizeof(unsigned long long)), "timeline alloc");
+    TB_CUDA(cudaMemsetAsync(g_pipe_tl.buf, 0, words * sizeof(unsigned long long), stream), "timeline");
+    g_pipe_tl.grid = grid;
+    p.timeline = g_pipe_tl.buf;
+  }
+#endif
   TB_CUDA(cudaLaunchKernel(pipe_kernel(), dim3((unsigned)grid), dim3(Cfg::THREADS), args, (size_t)cfg_smem(0), stream),
           "kernel launch (pipe)");
   g_launches.fetch_add(1, std::memory_order_relaxed);

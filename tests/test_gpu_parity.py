@@ -135,6 +135,48 @@ def test_large_row_sampled(tb, golden, oracle, n):
     assert rel <= NORMWISE
 
 
+def test_full_size_checksums(tb, oracle):
+    """Every element of a full-size product, in aggregate (algorithm-based
+    fault tolerance): column sums e^T C = (e^T A) B and row sums C e =
+    A (B e), the right-hand sides computed on the host (numpy, O(N^2)), for
+    the device entry and the host-buffer pipeline at N = 10000 (configs[3]).
+    A missing, doubled or misplaced tile, panel or strip moves a checksum by
+    ~1e-4 relative; rounding moves it by ~1e-16."""
+    import torch
+
+    n = 10000
+    a, b = oracle.generate(n, n, 11), oracle.generate(n, n, 12)
+    col_ref, row_ref = a.sum(axis=0) @ b, a @ b.sum(axis=1)
+    c, _ = tb.dgemm(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda())
+    for name, cc in (("device", c.cpu().numpy()), ("host", None)):
+        if cc is None:
+            cc = np.empty((n, n))
+            sec = np.zeros(1)
+            assert tb.gpu_tiled_multiply_flat(0, a, b, n, n, n, 32, cc, sec) == 0
+        assert oracle.normwise_rel(cc.sum(axis=0), col_ref) <= NORMWISE, name
+        assert oracle.normwise_rel(cc.sum(axis=1), row_ref) <= NORMWISE, name
+
+
+def test_n32768_checksums(tb):
+    """configs[4] size on one GPU: full-matrix column / row checksums of the
+    N = 32768 product (8.6 GB per matrix) against fp64 matrix-vector products
+    of the operands (cuBLAS DGEMV on the device; O(N^2))."""
+    import torch
+
+    n = 32768
+    g = torch.Generator(device="cuda").manual_seed(5)
+    a = torch.rand((n, n), dtype=torch.float64, device="cuda", generator=g) * 3 + 2
+    b = torch.rand((n, n), dtype=torch.float64, device="cuda", generator=g) * 3 + 2
+    c, _ = tb.dgemm(a, b)
+    col = c.sum(0)
+    row = c.sum(1)
+    del c
+    col_ref = a.sum(0) @ b
+    row_ref = a @ b.sum(1)
+    assert (torch.linalg.norm(col - col_ref) / torch.linalg.norm(col_ref)).item() <= NORMWISE
+    assert (torch.linalg.norm(row - row_ref) / torch.linalg.norm(row_ref)).item() <= NORMWISE
+
+
 def test_deterministic_bits(tb, oracle):
     a, b = _gen(oracle, 515, 515, 515, 3, 4)
     for v in FAST + ["paper"]:

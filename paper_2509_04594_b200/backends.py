@@ -222,6 +222,36 @@ def _with_transfers(timed, *args):
     return out, sec, tr
 
 
+_PINNED_OUT_MAX = 2 << 30   # bytes; larger outputs are plain numpy arrays
+_pinned_sizes: set = set()
+
+
+def _fresh_output(m: int, n: int) -> np.ndarray:
+    """A fresh m x n float64 numpy array for the MultiplyFn's product, backed
+    by page-locked memory from torch's caching host allocator.
+
+    The array is the caller's (it keeps its pinned tensor alive); when the
+    caller drops it the block returns to the allocator's cache and a later
+    call reuses it, already pinned and faulted in. So the D2H copies land in
+    the output directly instead of through the staging ring, and no call pays
+    first-touch page faults on a fresh 800 MB array (N = 10000: ~11 ms with
+    16 threads, profiles/r01_pageable_staging.txt). On the first call at a
+    size a second block is pinned and released at once, because harnesses
+    hold the previous output while making the next one (harness.py:204-217
+    keeps the last trial's product for verification). Outputs above 2 GB
+    stay plain numpy (bounded pinned footprint)."""
+    nbytes = m * n * 8
+    if nbytes > _PINNED_OUT_MAX:
+        return np.empty((m, n), dtype=np.float64)
+    torch = _torch()
+    out = torch.empty((m, n), dtype=torch.float64, pin_memory=True)
+    if nbytes not in _pinned_sizes:
+        _pinned_sizes.add(nbytes)
+        spare = torch.empty((m, n), dtype=torch.float64, pin_memory=True)
+        del spare  # a second block, cached by the host allocator for the next call
+    return out.numpy()
+
+
 def gpu_tiled_multiply(a, b, tile: TileConfig = TileConfig(), variant="auto", device=None) -> np.ndarray:
     """``MultiplyFn`` form (backends.py:56): fresh product, inputs untouched.
 
@@ -239,7 +269,7 @@ def gpu_tiled_multiply(a, b, tile: TileConfig = TileConfig(), variant="auto", de
         # tiny products: a plain upload / launch / download costs the same
         # (N = 500: 0.55 ms either way; N = 1000: 1.57 vs 0.92 ms staged)
         return gpu_tiled_multiply_timed(a, b, tile, variant, device)[0]
-    out = np.empty((m, n), dtype=np.float64)
+    out = _fresh_output(m, n)
     sec = np.zeros(1)
     _lib.check(gpu_tiled_multiply_flat(_device_index(device), a, b, m, k, n, tile.k, out, sec, variant=variant))
     return out

@@ -517,6 +517,32 @@ def test_multiplyfn_through_host_pipeline(tb, oracle):
         assert oracle.normwise_rel(c[rows], oracle.tiled_parallel(a[rows], b)) <= NORMWISE
 
 
+def test_multiplyfn_outputs_are_fresh_and_independent(tb, oracle):
+    """The MultiplyFn's product arrays come from a pinned-block cache: each
+    call returns a new, writable, C-contiguous array that the caller owns; a
+    held product is never reused or overwritten by later calls, and a
+    dropped one may be (backends.py:17-19: fresh output per call)."""
+    import torch
+
+    m = k = n = 1200
+    a, b = oracle.generate(m, k, 71), oracle.generate(k, n, 72)
+    ref = tb.gpu_tiled_multiply_timed(a, b)[0]
+    first = tb.gpu_tiled_multiply(a, b)
+    snap = first.copy()
+    assert first.flags["C_CONTIGUOUS"] and first.flags["WRITEABLE"] and first.dtype == np.float64
+    assert torch.from_numpy(first).is_pinned()
+    outs = [tb.gpu_tiled_multiply(a * (i + 2), b) for i in range(3)]
+    assert np.array_equal(first, snap), "a held product was overwritten by a later call"
+    ptrs = {o.ctypes.data for o in outs + [first]}
+    assert len(ptrs) == 4, "live products share memory"
+    for i, o in enumerate(outs):
+        assert oracle.normwise_rel(o, (i + 2) * ref) <= NORMWISE
+    first[:] = 0.0  # the caller may write its own array
+    del outs
+    again = tb.gpu_tiled_multiply(a, b)
+    assert oracle.normwise_rel(again, ref) <= NORMWISE
+
+
 def test_flat_repeated_varied_calls(tb, oracle):
     """Back-to-back host-buffer calls of varying size and buffer kind (pinned
     / pageable, pipelined / single-shot, ragged / aligned) reuse and regrow

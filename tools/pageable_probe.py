@@ -35,6 +35,16 @@ t = best(lambda: tb.gpu_tiled_multiply_flat(0, ap, bp, n, n, n, 32, cp, s))
 print(f"flat pinned        {t*1e3:8.1f} ms {f/t/1e12:6.2f} TFLOP/s")
 t = best(lambda: tb.gpu_tiled_multiply(a, b), reps=2)
 print(f"MultiplyFn (numpy) {t*1e3:8.1f} ms {f/t/1e12:6.2f} TFLOP/s")
+held = []
+
+
+def fn_held():  # a harness keeps the previous product while making the next one
+    held.append(tb.gpu_tiled_multiply(a, b))
+    del held[:-1]
+
+
+t = best(fn_held, reps=3)
+print(f"MultiplyFn, previous output held {t*1e3:8.1f} ms {f/t/1e12:6.2f} TFLOP/s")
 
 # output page-fault cost: the MultiplyFn allocates a fresh output per call
 import ctypes  # noqa: E402

@@ -157,13 +157,15 @@ TB_API const char* tb_last_error(void);
 TB_API const char* tb_version(void);
 
 /* The host-buffer pipeline's shape for an m x k x n call on a device with
- * `sms` SMs (no device work; tests and tooling): phase-1 rows *out_mq, whether
+ * `sms` SMs (no device work; tests and tooling); `staging` bit 0: A or B is
+ * pageable (staged through pinned slots), bit 1: C is pageable: phase-1 rows *out_mq, whether
  * phase 1 runs as the fused flag-driven launch, the K-panel bounds
  * out_panels[0..*out_npanels) (0 .. k) and the phase-2 row-block bounds
  * out_blocks[0..*out_nblocks) (*out_mq .. m). OVER_LIMITS (counts still set)
  * when the arrays are too small. Internal to tb_gpu_tiled_multiply_flat_ex;
  * no reference counterpart. */
-TB_API int tb_pipeline_plan(int64_t m, int64_t k, int64_t n, int32_t sms, int32_t fused_ok, int64_t* out_mq,
+TB_API int tb_pipeline_plan(int64_t m, int64_t k, int64_t n, int32_t sms, int32_t fused_ok,
+                            int32_t staging, int64_t* out_mq,
                             int32_t* out_fused, int64_t* out_panels, int32_t max_panels, int32_t* out_npanels,
                             int64_t* out_blocks, int32_t max_blocks, int32_t* out_nblocks);
 

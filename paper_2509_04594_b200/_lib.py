@@ -83,7 +83,8 @@ def _declare(l):
     _P32 = ctypes.POINTER(ctypes.c_int32)
     l.tb_kernel_launches.argtypes = []
     l.tb_kernel_launches.restype = ctypes.c_longlong
-    l.tb_pipeline_plan.argtypes = [_I64, _I64, _I64, _I32, _I32, _P64, _P32, _P64, _I32, _P32, _P64, _I32, _P32]
+    l.tb_pipeline_plan.argtypes = [_I64, _I64, _I64, _I32, _I32, _I32, _P64, _P32, _P64, _I32, _P32, _P64, _I32,
+                                   _P32]
     l.tb_dgemm_mgpu.argtypes = [_I32, _P32, _VP, _VP, _VP, _VP, _P64, _I64, _I64, _I32, _D, _D]
     l.tb_copy2d_async.argtypes = [_VP, _I64, _VP, _I64, _I64, _I64, _VP]
     for name in ("tb_copy2d_async", "tb_dgemm_mgpu", "tb_gpu_tiled_multiply_flat", "tb_gpu_tiled_multiply_flat_ex", "tb_dgemm", "tb_cublas_dgemm",
@@ -137,14 +138,16 @@ def kernel_launches() -> int:
     return int(lib().tb_kernel_launches())
 
 
-def pipeline_plan(m: int, k: int, n: int, sms: int = 148, fused_ok: bool = True) -> dict:
+def pipeline_plan(m: int, k: int, n: int, sms: int = 148, fused_ok: bool = True, staged: bool = False,
+                  staged_output: bool = False) -> dict:
     """Shape of the host-buffer pipeline tb_gpu_tiled_multiply_flat_ex would
     run for an m x k x n call (pure host computation; no device needed)."""
     mq, fused = ctypes.c_int64(), ctypes.c_int32()
     npan, nblk = ctypes.c_int32(), ctypes.c_int32()
     panels = (ctypes.c_int64 * 256)()
     blocks = (ctypes.c_int64 * 256)()
-    check(lib().tb_pipeline_plan(m, k, n, sms, 1 if fused_ok else 0, ctypes.byref(mq), ctypes.byref(fused), panels,
+    check(lib().tb_pipeline_plan(m, k, n, sms, 1 if fused_ok else 0, (1 if staged else 0) | (2 if staged_output else 0),
+                                 ctypes.byref(mq), ctypes.byref(fused), panels,
                                  256, ctypes.byref(npan), blocks, 256, ctypes.byref(nblk)))
     return {"mq": mq.value, "fused": bool(fused.value), "panels": list(panels[:npan.value]),
             "blocks": list(blocks[:nblk.value])}

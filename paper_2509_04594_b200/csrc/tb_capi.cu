@@ -170,7 +170,7 @@ int tb_gpu_tiled_multiply_flat_ex(int32_t device, const double* a, const double*
   const bool fused_ok = variant != TB_VARIANT_PAPER && variant != TB_VARIANT_DFMA &&
                         variant != TB_VARIANT_DMMA_CPASYNC && cfg_smem(0) <= g_dev[device].smem_optin &&
                         !direct_pageable;
-  const PipePlan plan = plan_pipeline(m, k, n, g_dev[device].sms, fused_ok);
+  const PipePlan plan = plan_pipeline(m, k, n, g_dev[device].sms, fused_ok, stage_a || stage_b, stage_c);
   const int64_t Mq = plan.Mq;
   bool fused = plan.fused;
   const std::vector<int64_t>& pk = plan.pk;  // phase-1 K-panel bounds
@@ -497,14 +497,15 @@ int tb_gpu_tiled_multiply_flat(int32_t device, const double* a, const double* b,
                                        out_seconds, nullptr);
 }
 
-int tb_pipeline_plan(int64_t m, int64_t k, int64_t n, int32_t sms, int32_t fused_ok, int64_t* out_mq,
+int tb_pipeline_plan(int64_t m, int64_t k, int64_t n, int32_t sms, int32_t fused_ok, int32_t staging,
+                     int64_t* out_mq,
                      int32_t* out_fused, int64_t* out_panels, int32_t max_panels, int32_t* out_npanels,
                      int64_t* out_blocks, int32_t max_blocks, int32_t* out_nblocks) {
   if (m < 1 || k < 1 || n < 1 || sms < 1 || !out_mq || !out_fused || !out_npanels || !out_nblocks) {
     set_err("bad pipeline-plan arguments");
     return TB_STATUS_BAD_DIMS;
   }
-  const PipePlan pl = plan_pipeline(m, k, n, sms, fused_ok != 0);
+  const PipePlan pl = plan_pipeline(m, k, n, sms, fused_ok != 0, (staging & 1) != 0, (staging & 2) != 0);
   *out_mq = pl.Mq;
   *out_fused = pl.fused ? 1 : 0;
   *out_npanels = (int32_t)pl.pk.size();

@@ -12,7 +12,17 @@ struct PipePlan {
   std::vector<int64_t> rb;     // phase-2 row-block bounds, rb[0] = Mq
 };
 
-PipePlan plan_pipeline(int64_t m, int64_t k, int64_t n, int sms, bool fused_ok) {
+// staged_inputs: A or B is pageable and goes through the pinned staging ring,
+// whose host copies share host DRAM bandwidth with the DMA: the effective
+// H2D rate is ~42 GB/s instead of 55, so phase 1 needs more rows to outlast
+// its transfers (N = 10000 numpy operands: Mq 5248 -> 7168 rows, 64.6 ->
+// 59.0 ms; profiles/r01_pipe_staged_mq.txt).
+// staged_output: C is pageable and drains through the same ring; the drain
+// (DMA into a slot, then the pool's copy out) runs at ~28 GB/s, so phase 1
+// must leave more rows to phase 2 (N = 10000 all-numpy: Mq 6144, 59.2 ms;
+// with the pinned-C cap 7168, 64.2 ms).
+PipePlan plan_pipeline(int64_t m, int64_t k, int64_t n, int sms, bool fused_ok, bool staged_inputs = false,
+                       bool staged_output = false) {
   PipePlan pl;
   int64_t& Mq = pl.Mq;
   bool& fused = pl.fused;
@@ -25,7 +35,8 @@ PipePlan plan_pipeline(int64_t m, int64_t k, int64_t n, int sms, bool fused_ok) 
   rb = {m};
   const double flops = 2.0 * (double)m * (double)n * (double)k;
   if (flops >= 1e11) {
-    constexpr double kH2D = 55e9, kRate = 36e12;  // B/s (PCIe gen5 x16, measured), flop/s (FP64 DMMA)
+    constexpr double kRate = 36e12;                       // flop/s (FP64 DMMA)
+    const double kH2D = staged_inputs ? 42e9 : 55e9;       // B/s (PCIe gen5 x16 / through staging, measured)
     const double den = (double)n * kH2D - 4.0 * kRate;
     int64_t mq = den > 0 ? (int64_t)(1.2 * 4.0 * kRate * (double)n / den) : m;
     int64_t kp0 = 256, kp_max = 2048, blk = 1536, groups = 2;
@@ -42,6 +53,16 @@ PipePlan plan_pipeline(int64_t m, int64_t k, int64_t n, int sms, bool fused_ok) 
       }
     }
     mq = (mq + 127) / 128 * 128;
+    // ... but leave phase 2 enough work to hide phase 1's C on its way back:
+    // Mq·n·8 bytes at the D2H rate <= (m - Mq)·n·2k flops at kRate, i.e.
+    // Mq <= m·c / (c + 1.2·8/D2H) with c = 2k/kRate and a x1.2 margin. Before
+    // the cap, N = 4000 / 6000 ran all rows in phase 1 and copied the whole
+    // C after the last GEMM: 7.66 / 18.4 ms pinned, now 6.59 / 15.2
+    // (profiles/r01_pipe_staged_mq.txt).
+    const double c2k = 2.0 * (double)k / kRate, kD2H = staged_output ? 28e9 : 53e9;
+    const int64_t mq_cap =
+        std::max<int64_t>(128, (int64_t)((double)m * c2k / (c2k + 1.2 * 8.0 / kD2H)) / 128 * 128);
+    if (!std::getenv("TB_PIPE")) mq = std::min(mq, mq_cap);
     // Phase 1 as one persistent launch that waits on per-panel flags (PIPE
     // mode) rather than a launch per panel and row group; TB_PIPE_FUSED=0
     // restores the launch-per-panel form (A/B).
@@ -56,7 +77,7 @@ PipePlan plan_pipeline(int64_t m, int64_t k, int64_t n, int sms, bool fused_ok) 
       const int64_t tn = (n + 127) / 128, P_sm = sms;
       int64_t best_r = mq / 128;
       double best_imb = 2.0;
-      for (int64_t rr = mq / 128; rr <= mq / 128 + 8 && rr * 128 < m - blk / 2; ++rr) {
+      for (int64_t rr = mq / 128; rr <= mq / 128 + 8 && rr * 128 < m - blk / 2 && rr * 128 <= mq_cap; ++rr) {
         const double per = (double)(rr * tn) / (double)P_sm;
         const double imb = std::ceil(per) - per;
         if (imb < best_imb - 1e-9) {

@@ -55,3 +55,17 @@ def test_random_shapes(seed):
 def test_bad_arguments():
     with pytest.raises(Exception):
         _lib.pipeline_plan(0, 10, 10)
+
+
+def test_staged_inputs_plan_more_phase1_rows():
+    """Staged (pageable) operands land at ~42 instead of 55 GB/s, so phase 1
+    must cover more rows to outlast its transfers."""
+    from paper_2509_04594_b200 import _lib
+
+    for n in (8000, 10000, 12000, 16384):
+        pinned = _lib.pipeline_plan(n, n, n)
+        staged = _lib.pipeline_plan(n, n, n, staged=True)
+        assert staged["mq"] > pinned["mq"]
+        assert staged["blocks"][0] == staged["mq"] and staged["blocks"][-1] == n
+        assert staged["panels"][0] == 0 and staged["panels"][-1] == n
+    assert _lib.pipeline_plan(10000, 10000, 10000, staged=True)["mq"] == 7168

@@ -3,6 +3,7 @@ TB_PIPE_TRACE=1 (tooling): per shape, the device intervals of every H2D / GEMM
 cell / D2H, the compute-idle gaps, and bare pinned-copy bandwidths.
 
     python tools/pipe_trace.py [N] [shape ...]      shape = default | R,P,Q
+    TRACE_PAGEABLE=1: pageable (numpy) A and B, pinned C
 """
 import json
 import os
@@ -18,6 +19,9 @@ g = torch.Generator().manual_seed(1)
 a = (torch.rand((n, n), dtype=torch.float64, generator=g) * 3 + 2).pin_memory()
 b = (torch.rand((n, n), dtype=torch.float64, generator=g) * 3 + 2).pin_memory()
 c = torch.empty((n, n), dtype=torch.float64).pin_memory()
+import os
+if os.environ.get("TRACE_PAGEABLE") == "1":  # numpy A, B (staged), pinned C: the MultiplyFn's case
+    a, b = a.numpy().copy(), b.numpy().copy()
 s, e = np.zeros(1), np.zeros(1)
 for i in range(3):
     print("CALL", i, file=sys.stderr, flush=True)

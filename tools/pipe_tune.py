@@ -4,6 +4,7 @@ rounds (tooling).
 
     python tools/pipe_tune.py N ROUNDS spec ...
     spec = default | VAR=value[;VAR=value]      e.g. TB_TAIL=128,384,768
+    TRACE_PAGEABLE=1 (as a spec or in the environment): numpy A and B; =2: numpy C too
 """
 import json
 import os
@@ -20,6 +21,11 @@ g = torch.Generator().manual_seed(1)
 a = (torch.rand((n, n), dtype=torch.float64, generator=g) * 3 + 2).pin_memory()
 b = (torch.rand((n, n), dtype=torch.float64, generator=g) * 3 + 2).pin_memory()
 c = torch.empty((n, n), dtype=torch.float64).pin_memory()
+import os
+if os.environ.get("TRACE_PAGEABLE") in ("1", "2"):  # numpy A, B (staged), pinned C: the MultiplyFn's case
+    a, b = a.numpy().copy(), b.numpy().copy()
+if os.environ.get("TRACE_PAGEABLE") == "2":  # numpy C too (the ctypes binding of INTEGRATION.md §1)
+    c = np.empty((n, n))
 s, e = np.zeros(1), np.zeros(1)
 es, ks = [], []
 for i in range(9):

@@ -480,9 +480,12 @@ def test_pageable_staging_matches_direct_copies(tb, oracle, monkeypatch, m, k, n
     the copy-thread pool; the product matches the plain pageable copies
     (TB_STAGE=0, which also takes the launch-per-panel phase 1, so a
     different k-split: normwise) and is bitwise the same when a pinned output
-    with pageable inputs (and the reverse) mixes both paths."""
+    with pageable inputs (and the reverse) mixes both paths. The plan's
+    phase-1 rows depend on which buffers are staged, so TB_PIPE pins one
+    shape for the bitwise comparisons."""
     import torch
 
+    monkeypatch.setenv("TB_PIPE", "2048,256,2048,1536")
     a, b = oracle.generate(m, k, 51), oracle.generate(k, n, 52)
     s = np.zeros(1)
     outs = []

@@ -333,7 +333,7 @@ def run_ours(args) -> None:
     out_s = np.zeros(1)
     e2e = np.zeros(1)
     e2e_times, e2e_dev = [], []
-    host_sharded = HostShardedGemm(panels=args.panels or 4) if world > 1 else None
+    host_sharded = HostShardedGemm(panels=args.panels or None) if world > 1 else None
     for i in range(1 + max(2, args.steps // 3)):
         if world > 1:
             dist.barrier()
@@ -420,7 +420,8 @@ def main():
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--variant", default="auto")
     p.add_argument("--panels", type=int, default=0,
-                   help="K-panels of the B broadcast at N>1 (0: geometric 128, x3, ... for the device path, 4 for the host path)")
+                   help="K-panels of the B exchange at N>1 (0: the default plans, geometric_panel_bounds for the device "
+                        "path and host_panel_bounds for the host path)")
     p.add_argument("--ref-seconds", type=float, default=10.0, help="CPU sample length per measurement (s)")
     p.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     p.add_argument("--dist-backend", default="nccl", help="torch.distributed backend at N>1 (nccl; gloo for tests)")

@@ -120,7 +120,10 @@ TB_API int tb_cublas_dgemm(const double* A, const double* B, double* C, int64_t 
  * not order itself after the caller's streams); synchronous.
  * out_kernel_seconds_max: max over devices of first-GEMM start .. last-GEMM
  * end (CUDA events); out_total_seconds (nullable): host clock around the
- * whole exchange + compute. variant: AUTO / DMMA_* / DFMA (not PAPER). */
+ * whole exchange + compute. variant: AUTO / DMMA_* / DFMA (not PAPER).
+ * No communicator handle (the tb_mgpu_init / tb_mgpu_destroy pair SURVEY.md
+ * §8(b) sketches): the exchange is peer copies on the library's per-device
+ * streams, so there is no NCCL state to own; tb_release frees the streams. */
 TB_API int tb_dgemm_mgpu(int32_t ndev, const int32_t* devices, const double* const* A_rows,
                          const double* B_root, double* const* B_replicas, double* const* C_rows,
                          const int64_t* rows, int64_t k, int64_t n, int32_t variant,

@@ -11,7 +11,10 @@ reference demos' `blas-numpy` backend (`a @ b`), and runs the reference's
 TrialRecord invariants and, at N = 1000, its `--verify` oracle check. The
 records are written with the reference's `write_records`.
 
-    python tools/reference_harness_e2e.py out.csv [trials]
+    python tools/reference_harness_e2e.py out.csv [trials] [--paper]
+
+--paper: the paper's grid N = 1000..10000 step 1000 (after the N = 1000
+verified run) instead of 2000 / 4000 / 10000.
 """
 import os
 import sys
@@ -32,8 +35,10 @@ import paper_2509_04594_b200 as tb  # noqa: E402
 
 
 def main():
-    out = sys.argv[1] if len(sys.argv) > 1 else "ref_harness.csv"
-    trials = int(sys.argv[2]) if len(sys.argv) > 2 else 5
+    args = [x for x in sys.argv[1:] if not x.startswith("--")]
+    out = args[0] if args else "ref_harness.csv"
+    trials = int(args[1]) if len(args) > 1 else 5
+    sizes = tuple(range(2000, 10001, 1000)) if "--paper" in sys.argv else (2000, 4000, 10000)
     reg = BackendRegistry()
     names = [d.name for d in tb.register_into(reg, BackendDescriptor)]
     assert names, "no CUDA device: register_into is a no-op"
@@ -44,7 +49,7 @@ def main():
     r1, meta = run_trials(RunConfig(backends=("gpu-tiled", "cublas-dgemm"), sizes=(1000,), trials=trials,
                                     verify=True), registry=reg)
     records += r1
-    r2, _ = run_trials(RunConfig(backends=("gpu-tiled", "cublas-dgemm", "blas-numpy"), sizes=(2000, 4000, 10000),
+    r2, _ = run_trials(RunConfig(backends=("gpu-tiled", "cublas-dgemm", "blas-numpy"), sizes=sizes,
                                  trials=trials), registry=reg)
     records += r2
     write_records(out, records, meta)

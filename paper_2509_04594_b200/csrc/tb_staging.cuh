@@ -112,8 +112,11 @@ class CopyPool {
 // rows over the pool.
 void pool_copy_rows(CopyPool& pool, char* dst, size_t dpitch, const char* src, size_t spitch, size_t width,
                     size_t rows) {
+  // 256 KB per part: one host thread copies ~4 GB/s, so a 5 MB panel slice
+  // split by MB kept only 5 of the 16 threads busy (staged panels at 14-25
+  // GB/s at N = 4000, below the 55 GB/s link).
   const size_t bytes = width * rows;
-  const int parts = (int)std::max<size_t>(1, std::min<size_t>((size_t)pool.threads(), bytes >> 20));
+  const int parts = (int)std::max<size_t>(1, std::min<size_t>(std::min<size_t>((size_t)pool.threads(), bytes >> 18), rows));
   pool.run(parts, [&](int i) {
     const size_t r0 = rows * i / parts, r1 = rows * (i + 1) / parts;
     if (dpitch == width && spitch == width) {

@@ -34,7 +34,14 @@ PipePlan plan_pipeline(int64_t m, int64_t k, int64_t n, int sms, bool fused_ok, 
   gb = {0, m};
   rb = {m};
   const double flops = 2.0 * (double)m * (double)n * (double)k;
-  if (flops >= 1e11) {
+  // Pipelined from 1e10 flops (N ~ 1700): N = 2000 / 3000 pinned 2.26 /
+  // 5.52 -> 1.95 / 3.72 ms; at N = 1000 the plain copy / GEMM / copy
+  // sequence stays faster (0.55 vs 0.60 ms; profiles/r01_pipe_min_flops.txt).
+  static const double min_flops = [] {  // TB_PIPE_MIN_FLOPS: tuning override
+    const char* e = std::getenv("TB_PIPE_MIN_FLOPS");
+    return e ? std::atof(e) : 1e10;
+  }();
+  if (flops >= min_flops) {
     constexpr double kRate = 36e12;                       // flop/s (FP64 DMMA)
     const double kH2D = staged_inputs ? 42e9 : 55e9;       // B/s (PCIe gen5 x16 / through staging, measured)
     const double den = (double)n * kH2D - 4.0 * kRate;

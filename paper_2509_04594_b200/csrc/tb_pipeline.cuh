@@ -103,6 +103,15 @@ PipePlan plan_pipeline(int64_t m, int64_t k, int64_t n, int sms, bool fused_ok, 
     const double tr_per_k = 8.0 * (double)(Mq + n) / kH2D, c_per_k = 2.0 * (double)Mq * (double)n / kRate;
     pk.assign(1, 0);
     double arrive = 0.0, finish = 0.0;
+    // Later panels are at least k / max_panels deep: when the transfers only
+    // just keep up (staged operands) the slack rule alone leaves every panel
+    // at kp0, and each panel costs the phase-1 launch an accumulating
+    // epilogue per tile (TB_PIPE_MAXP, 0 = no floor).
+    static const int64_t max_panels = [] {
+      const char* e = std::getenv("TB_PIPE_MAXP");
+      return e ? (int64_t)std::atoll(e) : (int64_t)0;
+    }();
+    const int64_t kp_floor = max_panels > 0 ? std::max<int64_t>(kp0, k / max_panels) : kp0;
     for (int64_t at = 0, step = kp0; at < k;) {
       int64_t nx = at + step >= k - step / 2 ? k : ((at + step) / kal * kal);
       if (nx <= at) nx = std::min<int64_t>(k, at + kal);
@@ -110,7 +119,7 @@ PipePlan plan_pipeline(int64_t m, int64_t k, int64_t n, int sms, bool fused_ok, 
       finish = std::max(finish, arrive) + c_per_k * (double)(nx - at);
       pk.push_back(nx);
       at = nx;
-      step = std::min<int64_t>(kp_max, std::max<int64_t>(kp0, (int64_t)((finish - arrive) / tr_per_k)));
+      step = std::min<int64_t>(kp_max, std::max<int64_t>(kp_floor, (int64_t)((finish - arrive) / tr_per_k)));
     }
     gb = (groups >= 2 && Mq >= 2048) ? std::vector<int64_t>{0, (Mq / 2 + 127) / 128 * 128, Mq}
                                      : std::vector<int64_t>{0, Mq};

@@ -255,7 +255,7 @@ class HostShardedGemm:
 
         # Uploads and gathers are issued from the copy stream, panel by panel:
         # NCCL orders gather q after the uploads enqueued before it (this
-        # rank's shares of panels <= q, and A after panel 0's share).
+        # rank's B shares and A column slices of panels <= q).
         works, off = [], 0
         with on(copy_s):
             if cuda:
@@ -272,7 +272,8 @@ class HostShardedGemm:
                                                          async_op=True))
                 off += sh
         if self.chunks:
-            step = -(-(-(-max(m, 1) // self.chunks)) // 128) * 128
+            step = -(-max(m, 1) // self.chunks)     # ceil(m / chunks) ...
+            step = -(-step // 128) * 128            # ... on 128-row tile bounds
             chunks = [(r0, min(m, r0 + step)) for r0 in range(0, m, step)]
         else:
             chunks = shrinking_chunks(m)

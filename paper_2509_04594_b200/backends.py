@@ -19,6 +19,7 @@ CPU path: without the library or a device these functions raise.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass
 from typing import Callable
 
@@ -223,7 +224,8 @@ def _with_transfers(timed, *args):
 
 
 _PINNED_OUT_MAX = 2 << 30   # bytes; larger outputs are plain numpy arrays
-_pinned_sizes: set = set()
+_PINNED_IDLE_MAX = 4 << 30  # bytes of pinned output blocks kept across sizes
+_pinned_sizes: set = set()  # sizes with two pinned blocks in the host allocator's cache
 
 
 def _fresh_output(m: int, n: int) -> np.ndarray:
@@ -235,21 +237,32 @@ def _fresh_output(m: int, n: int) -> np.ndarray:
     call reuses it, already pinned and faulted in. So the D2H copies land in
     the output directly instead of through the staging ring, and no call pays
     first-touch page faults on a fresh 800 MB array (N = 10000: ~11 ms with
-    16 threads, profiles/r01_pageable_staging.txt). On the first call at a
-    size a second block is pinned and released at once, because harnesses
-    hold the previous output while making the next one (harness.py:204-217
-    keeps the last trial's product for verification). Outputs above 2 GB
-    stay plain numpy (bounded pinned footprint)."""
+    16 threads, profiles/r01_pageable_staging.txt). The first call at a size
+    pins two blocks (two, because harnesses hold the previous output while
+    making the next one: harness.py:204-217 keeps the last trial's product
+    for verification): a one-time ~1.2 s at N = 10000, which the reference
+    harness's warm-up call absorbs (harness.py:201-203). Pinning happens here,
+    on the calling thread before the call's copies start: from a background
+    thread it stalled concurrent calls, and a background cudaFreeHost
+    deadlocked a staged call (whose phase-1 kernel waits on copies this
+    thread enqueues) into its 10 s trap. Outputs above 2 GB stay plain
+    numpy, as do all with TB_PINNED_OUTPUT=0; past 4 GB of such blocks
+    across sizes the allocator's idle blocks are released first."""
     nbytes = m * n * 8
-    if nbytes > _PINNED_OUT_MAX:
+    if nbytes > _PINNED_OUT_MAX or nbytes == 0 or os.environ.get("TB_PINNED_OUTPUT") == "0":
         return np.empty((m, n), dtype=np.float64)
     torch = _torch()
-    out = torch.empty((m, n), dtype=torch.float64, pin_memory=True)
     if nbytes not in _pinned_sizes:
+        held = sum(2 * (1 << (b - 1).bit_length()) for b in _pinned_sizes)
+        if _pinned_sizes and held + 2 * (1 << (nbytes - 1).bit_length()) > _PINNED_IDLE_MAX:
+            torch._C._host_emptyCache()  # frees idle cached pinned blocks only
+            _pinned_sizes.clear()
         _pinned_sizes.add(nbytes)
+        out = torch.empty((m, n), dtype=torch.float64, pin_memory=True)
         spare = torch.empty((m, n), dtype=torch.float64, pin_memory=True)
-        del spare  # a second block, cached by the host allocator for the next call
-    return out.numpy()
+        del spare  # the second block, cached by the host allocator for the next call
+        return out.numpy()
+    return torch.empty((m, n), dtype=torch.float64, pin_memory=True).numpy()
 
 
 def gpu_tiled_multiply(a, b, tile: TileConfig = TileConfig(), variant="auto", device=None) -> np.ndarray:

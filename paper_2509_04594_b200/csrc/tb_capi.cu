@@ -336,7 +336,7 @@ int tb_gpu_tiled_multiply_flat_ex(int32_t device, const double* a, const double*
   // the fused phase-1 launch first (its flags gate it), then per K-panel the
   // copies (+ the unfused form's panel GEMMs), then per row block its copy
   // and GEMM; the column strip once all of A has been enqueued.
-  if (fused) {
+  auto phase1 = [&]() -> int {
     // Phase 1: one persistent launch; its producer waits on each panel's flag.
     const cudaStream_t cs = css[0];
     TB_CUDA(cudaStreamWaitEvent(cs, evTab, 0), "stream wait");
@@ -345,10 +345,20 @@ int tb_gpu_tiled_multiply_flat_ex(int32_t device, const double* a, const double*
     kt0.push_back(t0);
     kt1.push_back(t1);
     TB_CUDA(cudaEventRecord(t0, cs), "event record");
-    if ((s = launch_pipe(device, dA, lda_d, dB, ldb_d, dC, ldc_d, Mq, k, n1, st.dtab + 128, st.dtab, P, cs))) return s;
+    int rc = launch_pipe(device, dA, lda_d, dB, ldb_d, dC, ldc_d, Mq, k, n1, st.dtab + 128, st.dtab, P, cs);
+    if (rc) return rc;
     TB_CUDA(cudaEventRecord(t1, cs), "event record");
-    if ((s = d2h(cs, 0, Mq, 0, n1))) return s;
-  }
+    return d2h(cs, 0, Mq, 0, n1);
+  };
+  // With pinned operands every panel copy and flag is enqueued (microseconds)
+  // before the flag-spinning launch, so the running kernel never depends on
+  // host progress: another thread's device-synchronising call (cudaFreeHost,
+  // ...) cannot block an enqueue the kernel is spinning on. Staged operands
+  // are enqueued while the pool fills slots (tens of ms), so there the launch
+  // goes first and the call must not overlap such calls from other threads
+  // (include/tbgpu.h).
+  const bool phase1_first = fused && (stage_a || stage_b);
+  if (phase1_first && (s = phase1())) return s;
   // H2D of phase-1 panels: A slice, then B rows; in fused mode then the
   // panel's flag, copied after its data on the same stream.
   for (int p = 0; p < P; ++p) {
@@ -367,6 +377,7 @@ int tb_gpu_tiled_multiply_flat_ex(int32_t device, const double* a, const double*
       }
     }
   }
+  if (fused && !phase1_first && (s = phase1())) return s;
   // The column strip needs all of A and B; it goes on the stream the last
   // row block does not use, after the block before it, so it overlaps the
   // last block instead of trailing it.

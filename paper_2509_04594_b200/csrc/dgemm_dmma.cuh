@@ -29,6 +29,10 @@
 // as one conflict-free 128-bit load per two steps, B fragments as
 // conflict-free 64-bit loads (derivation in DESIGN.md §4).
 #pragma once
+
+#ifndef TB_GROUP_M
+#define TB_GROUP_M 16  // tile-raster band height (A/B builds: tools/build_variant.py NAME -DTB_GROUP_M=16)
+#endif
 #include <cstdint>
 #include <type_traits>
 #include <cuda.h>
@@ -65,7 +69,7 @@ struct DmmaCfgT {
   static constexpr int B_STAGE = BK * BN * 8;  // 16 KB: 8 boxes of [16 k][16 n] swizzled
   static constexpr int STAGE = A_STAGE + B_STAGE;
   static constexpr int B_BOX = BK * 16 * 8;  // 2 KB
-  static constexpr int GROUP_M = 8;          // tile raster: GROUP_M tile-rows per band
+  static constexpr int GROUP_M = TB_GROUP_M; // tile raster: GROUP_M tile-rows per band
   static constexpr int TILE_ELEMS = BM * BN;
 };
 using DmmaCfg = DmmaCfgT<128>;

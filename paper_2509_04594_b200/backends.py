@@ -209,10 +209,19 @@ def gpu_tiled_multiply_timed(a, b, tile: TileConfig = TileConfig(), variant="aut
     clk.mark(1)
     out, sec = dgemm(ta, tb, tile_edge=tile.k, variant=variant)
     clk.mark(2)
-    host = out.cpu().numpy()
+    host = _download(out, torch)
     clk.mark(3)
     clk.finish(a.nbytes + b.nbytes, host.nbytes)
     return host, sec
+
+
+def _download(out, torch) -> np.ndarray:
+    """Device product -> fresh host numpy array: one DMA into a cached pinned
+    block when the size allows (``_fresh_output``), not a pageable copy
+    (N = 10000: 0.36 s at 2.2 GB/s through ``.cpu()``)."""
+    host = _fresh_output(out.shape[0], out.shape[1])
+    torch.from_numpy(host).copy_(out)
+    return host
 
 
 def _with_transfers(timed, *args):
@@ -299,7 +308,7 @@ def cublas_multiply_timed(a, b, device=None, transfers=None):
     clk.mark(1)
     out, sec = cublas_dgemm(ta, tb)
     clk.mark(2)
-    host = out.cpu().numpy()
+    host = _download(out, torch)
     clk.mark(3)
     clk.finish(a.nbytes + b.nbytes, host.nbytes)
     return host, sec

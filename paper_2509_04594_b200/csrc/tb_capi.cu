@@ -452,13 +452,17 @@ int tb_gpu_tiled_multiply_flat_ex(int32_t device, const double* a, const double*
   // The call is synchronous: spin on the last D2H's event rather than a
   // blocking wait, whose wake-up latency would add to every call.
   static const bool block_sync = std::getenv("TB_SYNC_BLOCK") != nullptr;
+  // A fault here in fused mode is most likely the phase-1 kernel's 10 s
+  // trap: a panel flag never landed (include/tbgpu.h).
+  const char* what = fused ? "kernel execution (fused phase 1: a panel that never landed traps after 10 s)"
+                           : "kernel execution";
   if (block_sync) {
-    TB_CUDA(cudaEventSynchronize(e_end), "kernel execution");
+    TB_CUDA(cudaEventSynchronize(e_end), what);
   } else {
     cudaError_t q;
     while ((q = cudaEventQuery(e_end)) == cudaErrorNotReady) {
     }
-    TB_CUDA(q, "kernel execution");
+    TB_CUDA(q, what);
   }
   for (cudaStream_t cs : css) TB_CUDA(cudaStreamSynchronize(cs), "kernel execution");
   const auto h_sync = std::chrono::steady_clock::now();

@@ -162,7 +162,9 @@ int tb_gpu_tiled_multiply_flat_ex(int32_t device, const double* a, const double*
   //  while the panels stream in (A's panel slice by a 2D copy, B's panel as
   //  contiguous rows). The first panel is small, so the GEMM starts early;
   //  Mq is sized so a panel's GEMM (2·Mq·kp·n flops) outlasts its transfer
-  //  (8·kp·(Mq+n) bytes) and compute does not wait on PCIe afterwards.
+  //  (8·kp·(Mq+n) bytes) and compute does not wait on PCIe afterwards,
+  //  capped so phase 2 still hides phase 1's C on its way back (the rates
+  //  depend on which buffers are staged; tb_pipeline.cuh).
   //  Phase 2 (row blocks): the remaining rows of A arrive as contiguous
   //  blocks and run full-K GEMMs; every finished part of C is copied back at
   //  once, and the last blocks shrink so the final D2H is short.

@@ -34,12 +34,13 @@ PipePlan plan_pipeline(int64_t m, int64_t k, int64_t n, int sms, bool fused_ok, 
   gb = {0, m};
   rb = {m};
   const double flops = 2.0 * (double)m * (double)n * (double)k;
-  // Pipelined from 1e10 flops (N ~ 1700): N = 2000 / 3000 pinned 2.26 /
-  // 5.52 -> 1.95 / 3.72 ms; at N = 1000 the plain copy / GEMM / copy
-  // sequence stays faster (0.55 vs 0.60 ms; profiles/r01_pipe_min_flops.txt).
+  // Pipelined from 3e9 flops (N ~ 1150): N = 1200 / 2000 / 3000 pinned
+  // 1.06 / 2.26 / 5.52 -> 0.94 / 1.84 / 3.52 ms; at N = 1000 the plain copy /
+  // GEMM / copy sequence stays faster (0.56 vs 0.68 ms;
+  // profiles/r01_pipe_min_flops.txt, r01_pipe_fused_threshold.txt).
   static const double min_flops = [] {  // TB_PIPE_MIN_FLOPS: tuning override
     const char* e = std::getenv("TB_PIPE_MIN_FLOPS");
-    return e ? std::atof(e) : 1e10;
+    return e ? std::atof(e) : 3e9;
   }();
   if (flops >= min_flops) {
     constexpr double kRate = 36e12;                       // flop/s (FP64 DMMA)
@@ -71,10 +72,15 @@ PipePlan plan_pipeline(int64_t m, int64_t k, int64_t n, int sms, bool fused_ok, 
         std::max<int64_t>(128, (int64_t)((double)m * c2k / (c2k + 1.2 * 8.0 / kD2H)) / 128 * 128);
     if (!std::getenv("TB_PIPE")) mq = std::min(mq, mq_cap);
     // Phase 1 as one persistent launch that waits on per-panel flags (PIPE
-    // mode) rather than a launch per panel and row group; TB_PIPE_FUSED=0
-    // restores the launch-per-panel form (A/B).
+    // mode) rather than a launch per panel and row group, from 2e11 flops:
+    // below that (N <= ~4600) the launch-per-panel form is as fast or faster
+    // (pinned N = 1200 / 2000 / 3000 / 4000: 0.95 / 1.85 / 3.52 / 6.31 ms vs
+    // fused 1.06 / 1.93 / 3.67 / 6.49), above it the fused launch wins
+    // (N = 5000 / 10000: 10.53 / 57.2 vs 10.75 / 59.9;
+    // profiles/r01_pipe_fused_threshold.txt). TB_PIPE_FUSED=0 / 1 forces
+    // either form (A/B).
     const char* fe = std::getenv("TB_PIPE_FUSED");
-    fused = fused_ok && !(fe && std::strcmp(fe, "0") == 0);
+    fused = fused_ok && (fe ? std::strcmp(fe, "0") != 0 : flops >= 2e11);
     if (fused && !std::getenv("TB_PIPE")) {
       // The fused launch gives CTA c the phase-1 tiles c, c + P, ...: pick
       // the tile-row count (>= the compute-cover minimum, up to 8 more) whose

@@ -79,8 +79,9 @@ TB_API int tb_gpu_tiled_multiply_flat(int32_t device, const double* a, const dou
  * the end of the last D2H copy (the `e2e` bench leg). Large calls run a
  * copy/compute pipeline (shape: tb_pipeline_plan);
  * out_seconds is then the union of the GEMM launches' intervals.
- * With pageable a or b (staged through pinned slots), a call's phase-1
- * kernel waits on copies this thread enqueues over the call: other threads
+ * With pageable a or b (staged through pinned slots) on a large call (fused
+ * phase 1, >= 2e11 flops), the phase-1 kernel waits on copies this thread
+ * enqueues over the call: other threads
  * must not issue device-synchronising calls (cudaFreeHost, cudaFree, ...) on
  * the same device meanwhile; if one blocks the enqueue, the kernel traps
  * after 10 s (status 4) rather than hanging. Pinned buffers have no such

@@ -47,7 +47,11 @@ PipePlan plan_pipeline(int64_t m, int64_t k, int64_t n, int sms, bool fused_ok, 
     const double kH2D = staged_inputs ? 42e9 : 55e9;       // B/s (PCIe gen5 x16 / through staging, measured)
     const double den = (double)n * kH2D - 4.0 * kRate;
     int64_t mq = den > 0 ? (int64_t)(1.2 * 4.0 * kRate * (double)n / den) : m;
-    int64_t kp0 = 256, kp_max = 2048, blk = 1536, groups = 2;
+    // Phase-2 row blocks of ~m/4 rows (512..1536, on tile bounds): smaller
+    // problems need finer blocks for their D2H to overlap (N = 2000: 1536-row
+    // blocks 1.85 ms, 512-row 1.66; profiles/r01_pipe_small_blocks.txt).
+    int64_t kp0 = 256, kp_max = 2048, groups = 2;
+    int64_t blk = std::min<int64_t>(1536, std::max<int64_t>(512, (m / 4 + 64) / 128 * 128));
     // TB_PIPE=mq,kp0,kp_max,blk[,groups] overrides the shape (tuning experiments).
     if (const char* e = std::getenv("TB_PIPE")) {
       long long a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 2;

@@ -269,6 +269,7 @@ int tb_gpu_tiled_multiply_flat_ex(int32_t device, const double* a, const double*
     return TB_STATUS_OK;
   };
   auto gemm = [&](cudaStream_t cs, int64_t r0, int64_t r1, int64_t k0, int64_t k1, bool acc) -> int {
+    if (r1 <= r0) return TB_STATUS_OK;  // empty phase 1 (Mq = 0)
     cudaEvent_t t0 = mk(cudaEventDefault), t1 = mk(cudaEventDefault);
     if (!t0 || !t1) return cuda_fail(cudaGetLastError(), "event create");
     kt0.push_back(t0);
@@ -290,6 +291,7 @@ int tb_gpu_tiled_multiply_flat_ex(int32_t device, const double* a, const double*
   };
   std::vector<D2HJob> djobs;
   auto d2h = [&](cudaStream_t cs, int64_t r0, int64_t r1, int64_t c0, int64_t c1) -> int {
+    if (r1 <= r0 || c1 <= c0) return TB_STATUS_OK;
     cudaEvent_t done = mk(cudaEventDisableTiming);
     if (!done) return cuda_fail(cudaGetLastError(), "event create");
     TB_CUDA(cudaEventRecord(done, cs), "event record");

@@ -34,13 +34,13 @@ PipePlan plan_pipeline(int64_t m, int64_t k, int64_t n, int sms, bool fused_ok, 
   gb = {0, m};
   rb = {m};
   const double flops = 2.0 * (double)m * (double)n * (double)k;
-  // Pipelined from 3e9 flops (N ~ 1150): N = 1200 / 2000 / 3000 pinned
-  // 1.06 / 2.26 / 5.52 -> 0.94 / 1.84 / 3.52 ms; at N = 1000 the plain copy /
-  // GEMM / copy sequence stays faster (0.56 vs 0.68 ms;
-  // profiles/r01_pipe_min_flops.txt, r01_pipe_fused_threshold.txt).
+  // Pipelined from 1e9 flops (N ~ 800): N = 1000 / 2000 / 3000 pinned
+  // 0.58 / 2.26 / 5.52 (one copy / GEMM / copy sequence) -> 0.50 / 1.59 /
+  // 3.49 ms (profiles/r01_pipe_min_flops.txt, r01_pipe_fused_threshold.txt,
+  // r01_pipe_small_blocks.txt).
   static const double min_flops = [] {  // TB_PIPE_MIN_FLOPS: tuning override
     const char* e = std::getenv("TB_PIPE_MIN_FLOPS");
-    return e ? std::atof(e) : 3e9;
+    return e ? std::atof(e) : 1e9;
   }();
   if (flops >= min_flops) {
     constexpr double kRate = 36e12;                       // flop/s (FP64 DMMA)
@@ -130,6 +130,17 @@ PipePlan plan_pipeline(int64_t m, int64_t k, int64_t n, int sms, bool fused_ok, 
       pk.push_back(nx);
       at = nx;
       step = std::min<int64_t>(kp_max, std::max<int64_t>(kp_floor, (int64_t)((finish - arrive) / tr_per_k)));
+    }
+    // Below 2e10 flops (N <~ 2150) there is no phase 1: B lands first (one
+    // copy) and every row of C comes from full-K row blocks whose copies and
+    // GEMMs overlap (pinned N = 1000 / 1500 / 2000: 0.58 / 0.96 / 1.66 ->
+    // 0.50 / 0.92 / 1.59 ms; from N = 3000 up the panel phase wins;
+    // profiles/r01_pipe_small_blocks.txt). TB_PIPE_MQ0=0 / 1 forces (A/B).
+    const char* m0e = std::getenv("TB_PIPE_MQ0");
+    const bool mq0 = m0e ? std::strcmp(m0e, "1") == 0 : flops < 2e10;
+    if (mq0 && !fused) {
+      Mq = 0;
+      pk = {0, k};
     }
     gb = (groups >= 2 && Mq >= 2048) ? std::vector<int64_t>{0, (Mq / 2 + 127) / 128 * 128, Mq}
                                      : std::vector<int64_t>{0, Mq};

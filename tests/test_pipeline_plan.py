@@ -12,13 +12,13 @@ def _check(m, k, n, sms=148, fused_ok=True):
     pan, blk, mq = p["panels"], p["blocks"], p["mq"]
     assert pan[0] == 0 and pan[-1] == k and all(a < b for a, b in zip(pan, pan[1:]))
     assert blk[0] == mq and blk[-1] == m and all(a < b for a, b in zip(blk, blk[1:]))
-    assert mq == m or (mq % 128 == 0 and 0 < mq < m)
+    assert mq == m or (mq % 128 == 0 and 0 <= mq < m)  # mq = 0: no phase 1 (small problems)
     align = 16 if p["fused"] else 2  # k-stage bounds for the fused PIPE launch, TMA (even k0) otherwise
     assert all(x % align == 0 for x in pan[1:-1])
     assert all(x % 128 == 0 for x in blk[1:-1])  # only the last row block may be ragged
     if not fused_ok:
         assert not p["fused"]
-    if 2.0 * m * n * k < 3e9:
+    if 2.0 * m * n * k < 1e9:
         assert (mq, pan, blk, p["fused"]) == (m, [0, k], [m], False)
     if p["fused"]:
         assert 2 <= len(pan) - 1 <= 120
@@ -35,8 +35,17 @@ def test_n10000_shape():
 
 
 def test_small_problems_are_single_shot():
-    for s in [(1, 1, 1), (1000, 1000, 1000), (3001, 2999, 2500), (100, 100000, 100)]:
+    for s in [(1, 1, 1), (700, 700, 700), (100, 1000, 100)]:
         _check(*s)
+
+
+def test_small_problems_have_no_phase_one():
+    """Below 2e10 flops, B lands first and all rows come from row blocks."""
+    for s in [(1000, 1000, 1000), (2000, 2000, 2000), (1001, 999, 1500)]:
+        p = _check(*s)
+        assert p["mq"] == 0 and p["panels"] == [0, s[1]] and not p["fused"] and len(p["blocks"]) > 2
+    p = _check(3001, 2999, 2500)
+    assert p["mq"] > 0
 
 
 def test_unfused_form():

@@ -427,6 +427,31 @@ def test_flat_pipeline_shapes(tb, oracle, monkeypatch, shape, fused):
     assert (torch.linalg.norm(got - ref) / torch.linalg.norm(ref)).item() <= NORMWISE
 
 
+@pytest.mark.parametrize("m,k,n", [(1000, 1000, 1000), (1001, 999, 1003), (129, 40000, 257), (2047, 1500, 3001)])
+@pytest.mark.parametrize("kind", ["pinned", "numpy"])
+def test_flat_small_no_phase_one(tb, oracle, m, k, n, kind):
+    """Calls between 1e9 and 2e10 flops skip phase 1 (B first, full-K row
+    blocks with overlapped copies): odd and skinny shapes, pinned and
+    pageable buffers, against the oracle's rows and cuBLAS."""
+    import torch
+
+    assert tb._lib.pipeline_plan(m, k, n, staged=kind == "numpy")["mq"] == 0
+    a, b = oracle.generate(m, k, 81), oracle.generate(k, n, 82)
+    if kind == "pinned":
+        ah, bh = torch.from_numpy(a).pin_memory(), torch.from_numpy(b).pin_memory()
+        c = torch.full((m, n), float("nan"), dtype=torch.float64).pin_memory()
+        cn = c.numpy()
+    else:
+        ah, bh, c = a, b, np.full((m, n), np.nan)
+        cn = c
+    s = np.zeros(1)
+    assert tb.gpu_tiled_multiply_flat(0, ah, bh, m, k, n, 32, c, s) == tb.STATUS_OK
+    ref, _ = tb.cublas_dgemm(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda())
+    assert oracle.normwise_rel(cn, ref.cpu().numpy()) <= NORMWISE
+    rows = np.r_[0:2, m // 2, m - 2:m]
+    assert oracle.normwise_rel(cn[rows], oracle.tiled_parallel(a[rows], b)) <= NORMWISE
+
+
 @pytest.mark.parametrize("m,k,n", [(2320, 600, 2320), (2336, 500, 2368), (2368, 300, 2340), (4001, 257, 3999)])
 def test_edge_strip_split(tb, oracle, m, k, n):
     """Large TMA products with ragged m / n run as a whole-tile launch plus

@@ -141,6 +141,9 @@ PipePlan plan_pipeline(int64_t m, int64_t k, int64_t n, int sms, bool fused_ok, 
     if (mq0 && !fused) {
       Mq = 0;
       pk = {0, k};
+      // ~256-row blocks here (N = 1000 / 1500 / 2000: 0.64 / 0.98 / 1.58 ->
+      // 0.60 / 0.95 / 1.53 ms against ~m/4; profiles/r01_pipe_small_blocks.txt)
+      if (!std::getenv("TB_PIPE")) blk = 256;
     }
     gb = (groups >= 2 && Mq >= 2048) ? std::vector<int64_t>{0, (Mq / 2 + 127) / 128 * 128, Mq}
                                      : std::vector<int64_t>{0, Mq};

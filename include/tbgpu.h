@@ -81,11 +81,16 @@ TB_API int tb_gpu_tiled_multiply_flat(int32_t device, const double* a, const dou
  * out_seconds is then the union of the GEMM launches' intervals.
  * With pageable a or b (staged through pinned slots) on a large call (fused
  * phase 1, >= 2e11 flops), the phase-1 kernel waits on copies this thread
- * enqueues over the call: other threads
- * must not issue device-synchronising calls (cudaFreeHost, cudaFree, ...) on
- * the same device meanwhile; if one blocks the enqueue, the kernel traps
- * after 10 s (status 4) rather than hanging. Pinned buffers have no such
- * window. */
+ * enqueues over the call: other threads should not issue device-synchronising
+ * calls (cudaFreeHost, cudaFree, ...) on the same device meanwhile. If one
+ * blocks the enqueue for longer than the flag-wait timeout (10 s;
+ * TB_PIPE_TIMEOUT_MS), the kernel aborts cleanly: the call returns
+ * TB_STATUS_RUNTIME (tb_last_error names the panel), out_c is not valid, and
+ * the CUDA context stays usable. Pinned buffers have no such window.
+ * out_seconds on the fused path is the union of the GEMM launch spans; the
+ * phase-1 launch's span includes its waits for panels still in flight, so it
+ * can exceed pure compute time when the copies lag (it is "kernel-only" in
+ * the reference's sense: no launch, copy or sync outside a kernel). */
 TB_API int tb_gpu_tiled_multiply_flat_ex(int32_t device, const double* a, const double* b,
                                   int64_t m, int64_t k, int64_t n, int32_t tile_edge,
                                   int32_t variant, double* out_c, int64_t out_c_len,
@@ -182,6 +187,25 @@ TB_API int tb_pipeline_plan(int64_t m, int64_t k, int64_t n, int32_t sms, int32_
 /* Number of kernels this library has launched so far in this process (its
  * own GEMM, strip, pipeline and staging kernels; not cuBLAS). */
 TB_API long long tb_kernel_launches(void);
+
+/* Run metadata (the reference's RunMetadata.capture hook, harness.py:126-142;
+ * SURVEY.md §5 "Metrics / logging") as one JSON object in buf (NUL
+ * terminated): this library's version and path, CUDA runtime / driver
+ * versions, the cuBLAS actually loaded (runtime version and file path — in a
+ * process that imported torch first it is torch's copy), its pinned math
+ * mode and FP64 emulation state, and for `device` (if present) the GPU name,
+ * SM count, compute capability, L2 / HBM size and max clocks.
+ * OVER_LIMITS when buf_len is too small. */
+TB_API int tb_runtime_info(int32_t device, char* buf, int64_t buf_len);
+
+/* The launches tb_dgemm would enqueue for a packed, 16-byte aligned
+ * m x k x n product on a device with `sms` SMs (no device work): a JSON array
+ * with, per launch, the kernel (dmma / dfma / paper), loader, CTA tile,
+ * sub-problem shape, grid and persistent schedule (data-parallel / stream-K /
+ * split-K shape, tiles, k-iterations per CTA, segments) and whether it is an
+ * edge strip. The "resolved variant / tile" of the run metadata. */
+TB_API int tb_launch_plan(int64_t m, int64_t k, int64_t n, int32_t variant, int32_t sms, char* buf,
+                          int64_t buf_len);
 
 /* Free the cached host-entry workspaces and cuBLAS handles. */
 TB_API void tb_release(void);

@@ -7,7 +7,7 @@ only as the checker / the timed CPU reference — never as the product path.
 It wraps ``oracle/tb_oracle.c`` (a C restatement of the reference's
 ``tilebench`` CPU kernels; see that file for per-function citations) and adds
 the reference's operand generator, which is numpy's PCG64 exactly as
-``/root/reference/pkg/src/tilebench/matrices.py:111-119`` calls it.
+``/root/reference/pkg/src/tilebench/matrices.py:50-58`` calls it.
 
 Parity pin: ``tests/golden/*`` were produced by importing the reference package
 itself (``tests/golden/make_golden.py``); ``tests/test_oracle.py`` checks every
@@ -77,14 +77,14 @@ def _operands(a, b):
 
 
 def generate(rows: int, cols: int, seed: int, lo: float = 2.0, hi: float = 5.0) -> np.ndarray:
-    """reference matrices.py:111-119: PCG64(seed).random((rows, cols)) scaled to [lo, hi]."""
+    """reference matrices.py:50-58: PCG64(seed).random((rows, cols)) scaled to [lo, hi]."""
     rng = np.random.Generator(np.random.PCG64(seed))
     u = rng.random((rows, cols))
     return lo + u * (hi - lo)
 
 
 def flop_count(n: int) -> int:
-    """reference matrices.py:122-131: exact 2n^3 - n^2 in Python ints."""
+    """reference matrices.py:61-70: exact 2n^3 - n^2 in Python ints."""
     n = int(n)
     return 2 * n**3 - n**2
 
@@ -137,7 +137,7 @@ def plan_partitions(num_tiles: int, threads: int) -> list[tuple[int, int]]:
 
 
 def max_abs_rel_diff(x, y) -> float:
-    """reference matrices.py:134-147."""
+    """reference matrices.py:73-86."""
     x = np.ascontiguousarray(x, dtype=np.float64)
     y = np.ascontiguousarray(y, dtype=np.float64)
     if x.shape != y.shape:

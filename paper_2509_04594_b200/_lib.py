@@ -42,7 +42,7 @@ EXPORTS = [
     "tb_gpu_tiled_multiply_flat", "tb_gpu_tiled_multiply_flat_ex", "tb_dgemm", "tb_dgemm_launch",
     "tb_cublas_dgemm", "tb_validate_launch", "tb_device_count", "tb_variant_name",
     "tb_resolve_variant", "tb_last_error", "tb_version", "tb_release", "tb_pipeline_plan",
-    "tb_kernel_launches", "tb_dgemm_mgpu", "tb_copy2d_async",
+    "tb_kernel_launches", "tb_dgemm_mgpu", "tb_copy2d_async", "tb_runtime_info", "tb_launch_plan",
 ]
 
 _D = ctypes.POINTER(ctypes.c_double)
@@ -87,7 +87,9 @@ def _declare(l):
                                    _P32]
     l.tb_dgemm_mgpu.argtypes = [_I32, _P32, _VP, _VP, _VP, _VP, _P64, _I64, _I64, _I32, _D, _D]
     l.tb_copy2d_async.argtypes = [_VP, _I64, _VP, _I64, _I64, _I64, _VP]
-    for name in ("tb_copy2d_async", "tb_dgemm_mgpu", "tb_gpu_tiled_multiply_flat", "tb_gpu_tiled_multiply_flat_ex", "tb_dgemm", "tb_cublas_dgemm",
+    l.tb_runtime_info.argtypes = [_I32, ctypes.c_char_p, _I64]
+    l.tb_launch_plan.argtypes = [_I64, _I64, _I64, _I32, _I32, ctypes.c_char_p, _I64]
+    for name in ("tb_runtime_info", "tb_launch_plan", "tb_copy2d_async", "tb_dgemm_mgpu", "tb_gpu_tiled_multiply_flat", "tb_gpu_tiled_multiply_flat_ex", "tb_dgemm", "tb_cublas_dgemm",
                  "tb_dgemm_launch", "tb_validate_launch", "tb_device_count", "tb_resolve_variant",
                  "tb_pipeline_plan"):
         getattr(l, name).restype = ctypes.c_int
@@ -151,6 +153,32 @@ def pipeline_plan(m: int, k: int, n: int, sms: int = 148, fused_ok: bool = True,
                                  256, ctypes.byref(npan), blocks, 256, ctypes.byref(nblk)))
     return {"mq": mq.value, "fused": bool(fused.value), "panels": list(panels[:npan.value]),
             "blocks": list(blocks[:nblk.value])}
+
+
+def _json_call(fn, *args) -> object:
+    import json
+
+    size = 4096
+    while True:
+        buf = ctypes.create_string_buffer(size)
+        st = fn(*args, buf, size)
+        if st == STATUS_OVER_LIMITS and size < (1 << 22):
+            size *= 4
+            continue
+        check(st)
+        return json.loads(buf.value.decode())
+
+
+def runtime_info(device: int | None = 0) -> dict:
+    """tb_runtime_info: library / CUDA / cuBLAS versions and paths, the pinned
+    cuBLAS math mode and the GPU's facts (run metadata, harness.py:126-142)."""
+    return _json_call(lib().tb_runtime_info, -1 if device is None else int(device))
+
+
+def launch_plan(m: int, k: int, n: int, variant="auto", sms: int = 148) -> list:
+    """tb_launch_plan: the launches (kernel, tile, grid, schedule) tb_dgemm
+    would enqueue for a packed m x k x n product (no device needed)."""
+    return _json_call(lib().tb_launch_plan, int(m), int(k), int(n), variant_id(variant), int(sms))
 
 
 def variant_id(variant) -> int:

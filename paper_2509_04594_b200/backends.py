@@ -323,7 +323,9 @@ def gpu_tiled_multiply_flat(device, a, b, m, k, n, tile_edge, out_c, out_seconds
     """gpuTiledMultiplyFlat (multiply.ts:54-79) over host buffers: numpy
     arrays (or pinned torch CPU tensors) in, status code out; ``out_c`` and
     ``out_seconds`` are caller-owned out-parameters. ``device=None`` ->
-    STATUS_NO_DEVICE, as for a null device in the reference."""
+    STATUS_NO_DEVICE, as for a null device in the reference. ``a``, ``b`` and
+    ``out_c`` must be C-contiguous float64 host buffers with exactly m*k,
+    k*n and m*n elements, else STATUS_BAD_DIMS (multiply.ts:66, :71-73)."""
 
     def ptr(x):
         if x is None:
@@ -335,12 +337,20 @@ def gpu_tiled_multiply_flat(device, a, b, m, k, n, tile_edge, out_c, out_seconds
     def length(x):
         return x.numel() if hasattr(x, "numel") else x.size
 
-    if device is None:
-        return _lib.STATUS_NO_DEVICE
+    def host_dense(x) -> bool:
+        # A C-contiguous float64 host buffer: the flat ABI reads plain
+        # row-major memory (multiply.ts:54-79 takes Float64Arrays).
+        if hasattr(x, "data_ptr"):  # torch tensor
+            return x.device.type == "cpu" and str(x.dtype) == "torch.float64" and x.is_contiguous()
+        return isinstance(x, np.ndarray) and x.dtype == np.float64 and x.flags["C_CONTIGUOUS"]
+
+    if device is None or not 0 <= int(device) < _lib.device_count():
+        return _lib.STATUS_NO_DEVICE  # multiply.ts:65: checked before the buffers
     for x in (a, b, out_c):
-        if hasattr(x, "dtype") and str(x.dtype) not in ("float64", "torch.float64"):
+        if not host_dense(x):
             return _lib.STATUS_BAD_DIMS
-    if length(out_seconds) < 1:
+    # executor.ts:86 -> multiply.ts:71-73: operand lengths must match the dims.
+    if length(a) != int(m) * int(k) or length(b) != int(k) * int(n) or length(out_seconds) < 1:
         return _lib.STATUS_BAD_DIMS
     sec = ctypes.c_double(0.0)
     e2e = ctypes.c_double(0.0)

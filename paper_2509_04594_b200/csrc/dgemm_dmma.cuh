@@ -106,15 +106,28 @@ struct GemmParams {
 // ptxas's allocation for the production kernel turned out to depend on):
 //   sk_tiles  -> number of K-panels Q
 //   counters  -> panel_it[Q + 1]: panel q covers k-stages [panel_it[q], panel_it[q+1])
-//   partials  -> panel_flags[Q] (int): panel q is usable once its flag != 0
-//                (written by the copy stream after the panel's copies).
+//   partials  -> panel_flags[kPipeFlagWords] (int): panel q is usable once
+//                flags[q] != 0 (written by the copy stream after the panel's
+//                copies); flags[kPipeAbortWord] is the launch's abort word
+//   sk_ipc    -> flag-wait timeout in milliseconds
 // Each CTA owns tiles blockIdx.x, +gridDim.x, ... and walks them
 // panel-major, accumulating into C for panels after the first.
+//
+// Abort instead of trap: a producer that waits longer than the timeout for a
+// panel flag (a host pipeline that stopped enqueueing, e.g. blocked behind
+// another thread's device-synchronising call) sets the abort word and, like
+// every producer that then sees the word, stops loading: it completes each
+// remaining stage's full barrier with a plain arrive (no bytes), so the
+// consumers run out their units on stale shared memory and the launch ends
+// normally. The host reads the word after the call and returns
+// TB_STATUS_RUNTIME; the CUDA context stays usable (a __trap would poison it
+// for the whole process). The host can also set the word to cut a launch short.
+constexpr int kPipeMaxPanels = 120;
+constexpr int kPipeAbortWord = 127;
+constexpr int kPipeFlagWords = 128;
 __device__ __forceinline__ int pipe_panels(const GemmParams& p) { return p.sk_tiles; }
 __device__ __forceinline__ const int* pipe_panel_it(const GemmParams& p) { return p.counters; }
-__device__ __forceinline__ const int* pipe_flags(const GemmParams& p) {
-  return reinterpret_cast<const int*>(p.partials);
-}
+__device__ __forceinline__ int* pipe_flags(const GemmParams& p) { return reinterpret_cast<int*>(p.partials); }
 
 #ifdef TB_TIMELINE
 __device__ __forceinline__ unsigned long long tl_now() {
@@ -242,16 +255,28 @@ __global__ void __launch_bounds__(DmmaCfg::THREADS, 1)
     Iter w(p);
     int tile, kb, ke;
     int ready_upto = 0;  // PIPE: panel flags observed set so far
+    bool aborted = false;  // PIPE: stop loading, complete the remaining stages empty
     while (w.next(p, tile, kb, ke)) {
       if constexpr (PIPE) {
         // Wait for the panel holding k-stages [kb, ke) (panels land in order).
-        while (ready_upto < pipe_panels(p) && pipe_panel_it(p)[ready_upto] <= kb) {
+        while (!aborted && ready_upto < pipe_panels(p) && pipe_panel_it(p)[ready_upto] <= kb) {
           if (ld_acquire_gpu(&pipe_flags(p)[ready_upto]) == 0) {
-            // Bounded: a panel that never lands (a broken host pipeline)
-            // faults the launch after ~10 s instead of hanging the device.
+            // Bounded: a panel that does not land within the timeout aborts
+            // the launch (see kPipeAbortWord) instead of hanging the device.
             const unsigned long long t_start = globaltimer_ns();
-            while (ld_acquire_gpu(&pipe_flags(p)[ready_upto]) == 0)
-              if (globaltimer_ns() - t_start > 10000000000ull) __trap();
+            const unsigned long long t_max = 1000000ull * (unsigned)p.sk_ipc;
+            int* abort_word = pipe_flags(p) + kPipeAbortWord;
+            while (ld_acquire_gpu(&pipe_flags(p)[ready_upto]) == 0) {
+              if (ld_acquire_gpu(abort_word) != 0) {
+                aborted = true;
+                break;
+              }
+              if (globaltimer_ns() - t_start > t_max) {
+                st_release_gpu(abort_word, 1 + ready_upto);  // 1 + the panel that never landed
+                aborted = true;
+                break;
+              }
+            }
             // tooling build: [grid][8] stamps, then [grid][4] producer flag waits
             // (total ns, count, panel-0 ns, last wait end)
             TB_TL(if (p.timeline) {
@@ -272,7 +297,9 @@ __global__ void __launch_bounds__(DmmaCfg::THREADS, 1)
       for (int kt = kb; kt < ke; ++kt) {
         mbar_wait(smem_u32(&empty[s]), ph ^ 1);  // fresh barrier: parity 1 reads as complete
         const uint32_t stage = smem_u32(smem + s * STAGE_BYTES);
-        if constexpr (LD == Loader::TMA) {
+        if (PIPE && aborted) {
+          mbar_arrive(smem_u32(&full[s]));  // aborted launch: release the stage with no bytes
+        } else if constexpr (LD == Loader::TMA) {
           const uint32_t fb = smem_u32(&full[s]);
           mbar_arrive_expect_tx(fb, STAGE_BYTES);  // OOB-filled boxes still count full bytes
 #pragma unroll

@@ -8,6 +8,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
+#include <dlfcn.h>
 
 #include <chrono>
 #include <cstdarg>
@@ -20,6 +21,7 @@
 #include <atomic>
 #include <map>
 #include <mutex>
+#include <string>
 
 #include "../../include/tbgpu.h"
 #include "dgemm_dmma.cuh"
@@ -243,19 +245,23 @@ int tb_gpu_tiled_multiply_flat_ex(int32_t device, const double* a, const double*
     if ((src == a && stage_a) || (src == b && stage_b)) {
       // Pageable source: fill pinned slots on the host (pool threads), then
       // DMA each slot; a slot is refilled once its previous copy completed.
-      const size_t w = (size_t)(c1 - c0) * sizeof(double);
-      const int64_t rows_per = std::max<int64_t>(1, (int64_t)(StageRing::kSlotBytes / w));
-      for (int64_t r = r0; r < r1; r += rows_per) {
-        const int64_t nr = std::min(rows_per, r1 - r);
-        const int i = ring.next;
-        ring.next = (ring.next + 1) % StageRing::kSlots;
-        TB_CUDA(cudaEventSynchronize(ring.ev[i]), "staging slot wait");
-        pool_copy_rows(*ring.pool, ring.slot[i], w, reinterpret_cast<const char*>(src + r * cols + c0), pitch, w,
-                       (size_t)nr);
-        TB_CUDA(cudaMemcpy2DAsync(dst + r * dld + c0, (size_t)dld * sizeof(double), ring.slot[i], w, w, (size_t)nr,
-                                  cudaMemcpyHostToDevice, hs),
-                "host to device copy");
-        TB_CUDA(cudaEventRecord(ring.ev[i], hs), "event record");
+      // Rows wider than a slot go in column chunks of at most one slot.
+      for (int64_t cc0 = c0; cc0 < c1; cc0 += StageRing::kSlotCols) {
+        const int64_t cc1 = std::min(c1, cc0 + StageRing::kSlotCols);
+        const size_t w = (size_t)(cc1 - cc0) * sizeof(double);
+        const int64_t rows_per = std::max<int64_t>(1, (int64_t)(StageRing::kSlotBytes / w));
+        for (int64_t r = r0; r < r1; r += rows_per) {
+          const int64_t nr = std::min(rows_per, r1 - r);
+          const int i = ring.next;
+          ring.next = (ring.next + 1) % StageRing::kSlots;
+          TB_CUDA(cudaEventSynchronize(ring.ev[i]), "staging slot wait");
+          pool_copy_rows(*ring.pool, ring.slot[i], w, reinterpret_cast<const char*>(src + r * cols + cc0), pitch, w,
+                         (size_t)nr);
+          TB_CUDA(cudaMemcpy2DAsync(dst + r * dld + cc0, (size_t)dld * sizeof(double), ring.slot[i], w, w,
+                                    (size_t)nr, cudaMemcpyHostToDevice, hs),
+                  "host to device copy");
+          TB_CUDA(cudaEventRecord(ring.ev[i], hs), "event record");
+        }
       }
     } else if (c0 == 0 && c1 == cols && dld == cols)
       TB_CUDA(cudaMemcpyAsync(dst + r0 * cols, src + r0 * cols, (size_t)(r1 - r0) * pitch, cudaMemcpyHostToDevice,
@@ -329,7 +335,10 @@ int tb_gpu_tiled_multiply_flat_ex(int32_t device, const double* a, const double*
       st.htab[256] = 1;
     }
     for (int q = 0; q <= P; ++q) st.htab[128 + q] = (int)((pk[q] + 15) / 16);
-    TB_CUDA(cudaMemcpyAsync(st.dtab, st.htab, (size_t)P * sizeof(int), cudaMemcpyHostToDevice, hs), "flags reset");
+    st.htab[kAbortReadback] = 0;
+    // Every flag and the abort word (tb::kPipeAbortWord) back to zero.
+    TB_CUDA(cudaMemcpyAsync(st.dtab, st.htab, tb::kPipeFlagWords * sizeof(int), cudaMemcpyHostToDevice, hs),
+            "flags reset");
     TB_CUDA(cudaMemcpyAsync(st.dtab + 128, st.htab + 128, (size_t)(P + 1) * sizeof(int), cudaMemcpyHostToDevice, hs),
             "panel table");
     if (!(evTab = mk(cudaEventDisableTiming))) return cuda_fail(cudaGetLastError(), "event create");
@@ -340,6 +349,26 @@ int tb_gpu_tiled_multiply_flat_ex(int32_t device, const double* a, const double*
   // the fused phase-1 launch first (its flags gate it), then per K-panel the
   // copies (+ the unfused form's panel GEMMs), then per row block its copy
   // and GEMM; the column strip once all of A has been enqueued.
+  // Test hook (tests/test_gpu_parity.py): TB_PIPE_TEST_WITHHOLD=q never sets
+  // panel q's flag, so the fused launch must abort on its flag-wait timeout.
+  const char* wh = std::getenv("TB_PIPE_TEST_WITHHOLD");
+  const int withhold = wh ? std::atoi(wh) : -1;
+  // Any error return after the fused launch is enqueued sets its abort word
+  // (on the H2D stream, which never waits on compute) and drains the call's
+  // streams, so no launch is left spinning on flags that will not come.
+  struct AbortGuard {
+    DeviceState& st;
+    cudaStream_t hs;
+    const cudaStream_t* css;
+    cudaStream_t ds;
+    bool armed = false, done = false;
+    ~AbortGuard() {
+      if (!armed || done) return;
+      cudaMemcpyAsync(st.dtab + tb::kPipeAbortWord, st.htab + 256, sizeof(int), cudaMemcpyHostToDevice, hs);
+      for (cudaStream_t x : {hs, css[0], css[1], ds}) cudaStreamSynchronize(x);
+      cudaGetLastError();
+    }
+  } abort_guard{st, hs, css, ds};
   auto phase1 = [&]() -> int {
     // Phase 1: one persistent launch; its producer waits on each panel's flag.
     const cudaStream_t cs = css[0];
@@ -349,9 +378,15 @@ int tb_gpu_tiled_multiply_flat_ex(int32_t device, const double* a, const double*
     kt0.push_back(t0);
     kt1.push_back(t1);
     TB_CUDA(cudaEventRecord(t0, cs), "event record");
-    int rc = launch_pipe(device, dA, lda_d, dB, ldb_d, dC, ldc_d, Mq, k, n1, st.dtab + 128, st.dtab, P, cs);
+    int rc = launch_pipe(device, dA, lda_d, dB, ldb_d, dC, ldc_d, Mq, k, n1, st.dtab + 128, st.dtab, P,
+                         pipe_timeout_ms(), cs);
     if (rc) return rc;
+    abort_guard.armed = true;
     TB_CUDA(cudaEventRecord(t1, cs), "event record");
+    // The launch's abort word, read back once the launch is done.
+    TB_CUDA(cudaMemcpyAsync(st.htab + kAbortReadback, st.dtab + tb::kPipeAbortWord, sizeof(int),
+                            cudaMemcpyDeviceToHost, cs),
+            "abort word readback");
     return d2h(cs, 0, Mq, 0, n1);
   };
   // With pinned operands every panel copy and flag is enqueued (microseconds)
@@ -370,7 +405,8 @@ int tb_gpu_tiled_multiply_flat_ex(int32_t device, const double* a, const double*
     if ((s = h2d(dB, ldb_d, b, n, pk[p], pk[p + 1], 0, n, "h2d_Bp", p))) return s;
     TB_CUDA(cudaEventRecord(evP[p], hs), "event record");
     if (fused) {
-      TB_CUDA(cudaMemcpyAsync(st.dtab + p, st.htab + 256, sizeof(int), cudaMemcpyHostToDevice, hs), "panel flag");
+      if (p != withhold)
+        TB_CUDA(cudaMemcpyAsync(st.dtab + p, st.htab + 256, sizeof(int), cudaMemcpyHostToDevice, hs), "panel flag");
     } else {
       // Phase 1, unfused: panel p of every row group once it has landed; row
       // group g stays on stream g, so its partial sums accumulate in panel order.
@@ -432,19 +468,22 @@ int tb_gpu_tiled_multiply_flat_ex(int32_t device, const double* a, const double*
     };
     for (const D2HJob& jb : djobs) {
       TB_CUDA(cudaStreamWaitEvent(ds, jb.ready, 0), "stream wait");
-      const size_t w = (size_t)(jb.c1 - jb.c0) * sizeof(double);
-      const int64_t rows_per = std::max<int64_t>(1, (int64_t)(StageRing::kSlotBytes / w));
-      for (int64_t r = jb.r0; r < jb.r1; r += rows_per) {
-        const int64_t nr = std::min(rows_per, jb.r1 - r);
-        if (inflight.size() - head == (size_t)StageRing::kSlots && (s = pop())) return s;
-        const int i = ring.next;
-        ring.next = (ring.next + 1) % StageRing::kSlots;
-        TB_CUDA(cudaStreamWaitEvent(ds, ring.ev[i], 0), "stream wait");  // the slot's last H2D has read it
-        TB_CUDA(cudaMemcpy2DAsync(ring.slot[i], w, dC + r * ldc_d + jb.c0, (size_t)ldc_d * sizeof(double), w,
-                                  (size_t)nr, cudaMemcpyDeviceToHost, ds),
-                "device to host copy");
-        TB_CUDA(cudaEventRecord(ring.ev[i], ds), "event record");
-        inflight.push_back({i, out_c + r * n + jb.c0, w, nr});
+      for (int64_t cc0 = jb.c0; cc0 < jb.c1; cc0 += StageRing::kSlotCols) {  // rows wider than a slot: chunks
+        const int64_t cc1 = std::min(jb.c1, cc0 + StageRing::kSlotCols);
+        const size_t w = (size_t)(cc1 - cc0) * sizeof(double);
+        const int64_t rows_per = std::max<int64_t>(1, (int64_t)(StageRing::kSlotBytes / w));
+        for (int64_t r = jb.r0; r < jb.r1; r += rows_per) {
+          const int64_t nr = std::min(rows_per, jb.r1 - r);
+          if (inflight.size() - head == (size_t)StageRing::kSlots && (s = pop())) return s;
+          const int i = ring.next;
+          ring.next = (ring.next + 1) % StageRing::kSlots;
+          TB_CUDA(cudaStreamWaitEvent(ds, ring.ev[i], 0), "stream wait");  // the slot's last H2D has read it
+          TB_CUDA(cudaMemcpy2DAsync(ring.slot[i], w, dC + r * ldc_d + cc0, (size_t)ldc_d * sizeof(double), w,
+                                    (size_t)nr, cudaMemcpyDeviceToHost, ds),
+                  "device to host copy");
+          TB_CUDA(cudaEventRecord(ring.ev[i], ds), "event record");
+          inflight.push_back({i, out_c + r * n + cc0, w, nr});
+        }
       }
     }
     TB_CUDA(cudaEventRecord(e_end, ds), "event record");
@@ -456,10 +495,7 @@ int tb_gpu_tiled_multiply_flat_ex(int32_t device, const double* a, const double*
   // The call is synchronous: spin on the last D2H's event rather than a
   // blocking wait, whose wake-up latency would add to every call.
   static const bool block_sync = std::getenv("TB_SYNC_BLOCK") != nullptr;
-  // A fault here in fused mode is most likely the phase-1 kernel's 10 s
-  // trap: a panel flag never landed (include/tbgpu.h).
-  const char* what = fused ? "kernel execution (fused phase 1: a panel that never landed traps after 10 s)"
-                           : "kernel execution";
+  const char* what = "kernel execution";
   if (block_sync) {
     TB_CUDA(cudaEventSynchronize(e_end), what);
   } else {
@@ -469,7 +505,14 @@ int tb_gpu_tiled_multiply_flat_ex(int32_t device, const double* a, const double*
     TB_CUDA(q, what);
   }
   for (cudaStream_t cs : css) TB_CUDA(cudaStreamSynchronize(cs), "kernel execution");
+  abort_guard.done = true;
   const auto h_sync = std::chrono::steady_clock::now();
+  if (fused && st.htab[kAbortReadback] != 0) {
+    set_err("kernel execution: fused phase-1 launch aborted, K-panel %d's flag not observed within %d ms "
+            "(was this thread blocked while enqueueing? include/tbgpu.h); the product is invalid",
+            st.htab[kAbortReadback] - 1, pipe_timeout_ms());
+    return TB_STATUS_RUNTIME;
+  }
 #ifdef TB_TIMELINE
   pipe_timeline_report();
 #endif
@@ -559,6 +602,135 @@ int tb_copy2d_async(void* dst, int64_t dpitch_bytes, const void* src, int64_t sp
 }
 
 long long tb_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
+
+namespace {
+void json_str(std::string& js, const char* key, const char* val) {
+  js += "\"";
+  js += key;
+  js += "\":";
+  if (!val) {
+    js += "null,";
+    return;
+  }
+  js += "\"";
+  for (const char* c = val; *c; ++c) {
+    if (*c == '"' || *c == '\\') js += '\\';
+    if ((unsigned char)*c >= 0x20) js += *c;
+  }
+  js += "\",";
+}
+void json_num(std::string& js, const char* key, long long v) {
+  js += "\"";
+  js += key;
+  js += "\":" + std::to_string(v) + ",";
+}
+int json_out(std::string& js, char* buf, int64_t len) {
+  if (!js.empty() && js.back() == ',') js.pop_back();
+  if ((int64_t)js.size() + 1 > len) {
+    set_err("buffer of %lld bytes too small for %lld bytes of JSON", (long long)len, (long long)js.size() + 1);
+    return TB_STATUS_OVER_LIMITS;
+  }
+  std::memcpy(buf, js.c_str(), js.size() + 1);
+  return TB_STATUS_OK;
+}
+const char* loaded_from(const void* sym) {
+  Dl_info di;
+  return dladdr(sym, &di) && di.dli_fname ? di.dli_fname : nullptr;
+}
+}  // namespace
+
+int tb_runtime_info(int32_t device, char* buf, int64_t buf_len) {
+  if (!buf || buf_len < 3) {
+    set_err("null or tiny output buffer");
+    return TB_STATUS_BAD_DIMS;
+  }
+  std::string js = "{";
+  json_str(js, "library", TB_VERSION);
+  json_str(js, "library_path", loaded_from((const void*)&tb_runtime_info));
+  int rt = 0, drv = 0;
+  if (cudaRuntimeGetVersion(&rt) != cudaSuccess) cudaGetLastError();
+  if (cudaDriverGetVersion(&drv) != cudaSuccess) cudaGetLastError();
+  json_num(js, "cuda_runtime_version", rt);
+  json_num(js, "cuda_driver_version", drv);
+  json_num(js, "cuda_runtime_header_version", CUDART_VERSION);
+  // The cuBLAS that is actually loaded: in a process that imported torch
+  // first, the dynamic linker binds libcublas.so.12 to torch's wheel copy,
+  // not the toolkit's (same soname), so report the runtime version and path.
+  int cmaj = -1, cmin = -1, cpat = -1;
+  cublasGetProperty(MAJOR_VERSION, &cmaj);
+  cublasGetProperty(MINOR_VERSION, &cmin);
+  cublasGetProperty(PATCH_LEVEL, &cpat);
+  char ver[64];
+  std::snprintf(ver, sizeof(ver), "%d.%d.%d", cmaj, cmin, cpat);
+  json_str(js, "cublas_version", ver);
+  json_num(js, "cublas_header_version", CUBLAS_VERSION);
+  const char* cub_path = loaded_from((const void*)&cublasCreate_v2);
+  json_str(js, "cublas_path", cub_path);
+  // FP64 emulation: cuBLAS 12.x's emulation API and its math-mode bits
+  // cover FP32 (BF16x9) only; probe the API by name (absent before 12.9).
+  void* h = cub_path ? dlopen(cub_path, RTLD_NOLOAD | RTLD_LAZY) : nullptr;
+  using GetEmu = int (*)(cublasHandle_t, int*);
+  GetEmu get_emu = h ? reinterpret_cast<GetEmu>(dlsym(h, "cublasGetEmulationStrategy")) : nullptr;
+  json_str(js, "cublas_emulation_strategy_env", std::getenv("CUBLAS_EMULATION_STRATEGY"));
+  json_str(js, "fp64_emulation", "none: no FP64 emulation in cuBLAS 12.x (emulation enums are FP32-only)");
+  const int count = device_count_raw();
+  json_num(js, "device_count", count);
+  if (device >= 0 && device < count && device < kMaxDevices) {
+    DeviceGuard guard(device);
+    cudaDeviceProp pr;
+    if (cudaGetDeviceProperties(&pr, device) == cudaSuccess) {
+      json_num(js, "device", device);
+      json_str(js, "gpu_name", pr.name);
+      json_num(js, "sm_count", pr.multiProcessorCount);
+      json_num(js, "compute_capability", pr.major * 10 + pr.minor);
+      json_num(js, "l2_bytes", pr.l2CacheSize);
+      json_num(js, "hbm_bytes", (long long)pr.totalGlobalMem);
+      json_num(js, "smem_optin_bytes", (long long)pr.sharedMemPerBlockOptin);
+      int clk = 0, mclk = 0;
+      cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, device);
+      cudaDeviceGetAttribute(&mclk, cudaDevAttrMemoryClockRate, device);
+      json_num(js, "sm_clock_max_khz", clk);
+      json_num(js, "mem_clock_max_khz", mclk);
+    } else {
+      cudaGetLastError();
+    }
+    if (ensure_cublas(device) == TB_STATUS_OK) {
+      cublasMath_t mode = CUBLAS_DEFAULT_MATH;
+      cublasGetMathMode(g_dev[device].cublas, &mode);
+      json_num(js, "cublas_math_mode", (int)mode);
+      json_str(js, "cublas_math_mode_name", mode == CUBLAS_DEFAULT_MATH ? "CUBLAS_DEFAULT_MATH" : "other");
+      int emu = -1;
+      if (get_emu && get_emu(g_dev[device].cublas, &emu) == 0)
+        json_num(js, "cublas_emulation_strategy", emu);
+      else
+        json_str(js, "cublas_emulation_strategy", nullptr);
+    }
+  }
+  if (h) dlclose(h);
+  if (js.back() == ',') js.pop_back();
+  js += "}";
+  return json_out(js, buf, buf_len);
+}
+
+int tb_launch_plan(int64_t m, int64_t k, int64_t n, int32_t variant, int32_t sms, char* buf, int64_t buf_len) {
+  if (m < 1 || k < 1 || n < 1 || sms < 1 || variant < 0 || variant >= TB_NUM_VARIANTS || !buf || buf_len < 3) {
+    set_err("bad launch-plan arguments");
+    return TB_STATUS_BAD_DIMS;
+  }
+  PlanRec rec;
+  rec.sms = sms;
+  rec.json = "[";
+  g_plan = &rec;
+  // Packed, 16-byte aligned operands (torch CUDA tensors); nothing is read.
+  const double* fake = reinterpret_cast<const double*>(256);
+  const int s = launch(0, fake, k, fake, n, const_cast<double*>(fake), n, m, k, n, 0, TB_DEFAULT_TILE_EDGE, variant,
+                       nullptr);
+  g_plan = nullptr;
+  if (s) return s;
+  if (rec.json.back() == ',') rec.json.pop_back();
+  rec.json += "]";
+  return json_out(rec.json, buf, buf_len);
+}
 
 void tb_release(void) {
   const int count = device_count_raw();

@@ -6,6 +6,16 @@
 
 namespace {
 
+// Dry-run recorder (tb_launch_plan): while set on this thread, launch() and
+// launch_tiles() describe the launches they would enqueue (JSON objects
+// appended to `json`) on a device with `sms` SMs instead of enqueueing them.
+struct PlanRec {
+  std::string json;
+  int sms = 148;
+};
+thread_local PlanRec* g_plan = nullptr;
+int dev_sms(int dev) { return g_plan ? g_plan->sms : g_dev[dev].sms; }
+
 // Persistent schedule (dgemm_dmma.cuh): data-parallel tiles round-robin over
 // the CTAs, then a stream-K region whose k-iterations are split evenly across
 // them. Three shapes, chosen on the host (the kernel is the same):
@@ -174,13 +184,28 @@ int launch_tiles(int dev, const double* A, int64_t lda, const double* B, int64_t
 // launch, A/B).
 int launch(int dev, const double* A, int64_t lda, const double* B, int64_t ldb, double* Cm, int64_t ldc, int64_t m,
            int64_t k, int64_t n, int accumulate, int tile_edge, int variant, cudaStream_t stream) {
-  int s = ensure_kernel_attrs(dev);
+  int s = g_plan ? TB_STATUS_OK : ensure_kernel_attrs(dev);
   if (s) return s;
+  // Per device: a staged call's re-pitch and GEMM are enqueued together, so
+  // two host threads on one stream cannot interleave repitch(A1), repitch(A2),
+  // gemm1, gemm2 on the shared stream-keyed staging buffer.
+  std::unique_lock<std::mutex> stage_lk(g_dev[dev].stage_mu, std::defer_lock);
   if (variant == TB_VARIANT_AUTO && !tma_ok(A, lda, B, ldb) && 2.0 * (double)m * (double)n * (double)k >= kStageMinFlops) {
     const bool sa = misaligned(A, lda), sb = misaligned(B, ldb);
     const int64_t lda2 = (k + 1) & ~int64_t(1), ldb2 = (n + 1) & ~int64_t(1);
     const size_t ea = sa ? (size_t)(m * lda2 + 32) : 0, eb = sb ? (size_t)(k * ldb2) : 0;
-    if ((ea + eb) * sizeof(double) <= kStageMaxBytes) {
+    if ((ea + eb) * sizeof(double) <= kStageMaxBytes && g_plan) {
+      g_plan->json += std::string("{\"repitch\":\"") + (sa ? "A" : "") + (sb ? "B" : "") + "\"},";
+      if (sa) {
+        A = reinterpret_cast<const double*>(256);
+        lda = lda2;
+      }
+      if (sb) {
+        B = reinterpret_cast<const double*>(256);
+        ldb = ldb2;
+      }
+    } else if ((ea + eb) * sizeof(double) <= kStageMaxBytes) {
+      stage_lk.lock();
       double* buf = nullptr;
       if ((s = stage_workspace(dev, stream, ea + eb + 32, &buf))) return s;
       double* a2 = buf;
@@ -207,7 +232,7 @@ int launch(int dev, const double* A, int64_t lda, const double* B, int64_t ldb, 
                                                       : wr <= 64 ? kStrip128x64 : kStripNone;
     const int64_t m1 = bcfg != kStripNone ? m - hb : m, n1 = rcfg != kStripNone ? n - wr : n;
     if ((bcfg != kStripNone || rcfg != kStripNone) && m1 >= 128 && n1 >= 128 &&
-        choose_bm(m1, n1, g_dev[dev].sms, false) == 128) {
+        choose_bm(m1, n1, dev_sms(dev), false) == 128) {
       // Main part on whole 128 x 128 tiles, then the right strip (all rows)
       // and the bottom strip (the main part's columns); disjoint parts of C.
       if ((s = launch_tiles(dev, A, lda, B, ldb, Cm, ldc, m1, k, n1, accumulate, tile_edge, variant, stream, -1)))
@@ -236,6 +261,13 @@ int launch_tiles(int dev, const double* A, int64_t lda, const double* B, int64_t
     const int K = tile_edge;
     dim3 block(K, K);
     dim3 grid((unsigned)((n + K - 1) / K), (unsigned)((m + K - 1) / K));
+    if (g_plan) {
+      char b[256];
+      std::snprintf(b, sizeof(b), "{\"kernel\":\"paper\",\"m\":%lld,\"n\":%lld,\"k\":%lld,\"block\":[%d,%d],"
+                    "\"grid\":[%u,%u]},", (long long)m, (long long)n, (long long)k, K, K, grid.x, grid.y);
+      g_plan->json += b;
+      return TB_STATUS_OK;
+    }
     tb::dgemm_paper_kernel<<<grid, block, 2 * K * K * sizeof(double), stream>>>(
         A, lda, B, ldb, Cm, ldc, (int)m, (int)k, (int)n, K, accumulate);
     g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -254,7 +286,7 @@ int launch_tiles(int dev, const double* A, int64_t lda, const double* B, int64_t
     const bool dfma = variant == TB_VARIANT_DFMA;
     const StripInfo si = strip > 0 ? strip_info(strip) : StripInfo{0, 0, 1, nullptr, 0};
     const bool narrow = si.fn != nullptr;  // an edge-strip shape (TMA only)
-    const int bm = narrow ? si.bm : strip == kStrip64x128 ? 64 : strip < 0 ? 128 : choose_bm(m, n, g_dev[dev].sms, dfma);
+    const int bm = narrow ? si.bm : strip == kStrip64x128 ? 64 : strip < 0 ? 128 : choose_bm(m, n, dev_sms(dev), dfma);
     const int bn = narrow ? si.bn : Cfg::BN;
     p.tiles_m = (int)((m + bm - 1) / bm);
     p.tiles_n = (int)((n + bn - 1) / bn);
@@ -269,7 +301,7 @@ int launch_tiles(int dev, const double* A, int64_t lda, const double* B, int64_t
     const int64_t kstage = narrow ? (int64_t)Cfg::BK * si.sub : bm == 64 ? (int64_t)Cfg::BK
                                                                        : (int64_t)Cfg::BK * kCfgs[cfg].sub;
     p.num_k = (int)((k + kstage - 1) / kstage);
-    const Schedule sc = plan_schedule(tiles, p.num_k, g_dev[dev].sms);
+    const Schedule sc = plan_schedule(tiles, p.num_k, dev_sms(dev));
     p.num_k = sc.num_k;  // split-K pads the k-slab count (extra slabs read as zeros)
     p.dp_tiles = sc.dp;
     p.sk_tiles = sc.sk;
@@ -277,6 +309,21 @@ int launch_tiles(int dev, const double* A, int64_t lda, const double* B, int64_t
     p.max_seg = sc.max_seg;
     p.partials = nullptr;
     p.counters = nullptr;
+    if (g_plan) {
+      const bool tma = variant == TB_VARIANT_DMMA_TMA || (dfma && tma_ok(A, lda, B, ldb));
+      const char* shape = sc.sk == 0 ? "data-parallel" : sc.dp == 0 && sc.grid != dev_sms(dev) ? "split-k"
+                                                                                                 : "stream-k";
+      char b[512];
+      std::snprintf(b, sizeof(b),
+                    "{\"kernel\":\"%s\",\"loader\":\"%s\",\"tile\":[%d,%d,%d],\"m\":%lld,\"n\":%lld,"
+                    "\"k\":%lld,\"grid\":%d,\"schedule\":\"%s\",\"dp_tiles\":%d,\"sk_tiles\":%d,"
+                    "\"sk_iters_per_cta\":%d,\"max_segments\":%d,\"k_stages\":%d,\"strip\":%s},",
+                    dfma ? "dfma" : "dmma", tma ? "tma" : "cp.async", bm, bn, (int)kstage, (long long)m,
+                    (long long)n, (long long)k, sc.grid, shape, sc.dp, sc.sk, sc.ipc, sc.max_seg, sc.num_k,
+                    narrow ? "true" : "false");
+      g_plan->json += b;
+      return TB_STATUS_OK;
+    }
 #ifdef TB_TIMELINE
     unsigned long long* tl_buf = nullptr;
     p.timeline = nullptr;
@@ -397,8 +444,17 @@ void pipe_timeline_report() {
 }
 #endif
 
+// Flag-wait timeout of the fused phase-1 launch (ms; after it the launch
+// aborts, dgemm_dmma.cuh kPipeAbortWord). TB_PIPE_TIMEOUT_MS overrides
+// (read per call: the abort test shortens it in-process).
+int pipe_timeout_ms() {
+  const char* e = std::getenv("TB_PIPE_TIMEOUT_MS");
+  const long v = e ? std::atol(e) : 0;
+  return v > 0 && v < 3600000 ? (int)v : 10000;
+}
+
 int launch_pipe(int dev, const double* A, int64_t lda, const double* B, int64_t ldb, double* Cm, int64_t ldc,
-                int64_t m, int64_t k, int64_t n, const int* panel_it_d, const int* flags_d, int Q,
+                int64_t m, int64_t k, int64_t n, const int* panel_it_d, int* flags_d, int Q, int timeout_ms,
                 cudaStream_t stream) {
   int s = ensure_kernel_attrs(dev);
   if (s) return s;
@@ -422,16 +478,16 @@ int launch_pipe(int dev, const double* A, int64_t lda, const double* B, int64_t 
   const int64_t tiles = (int64_t)p.tiles_m * p.tiles_n;
   p.dp_tiles = (int)tiles;
   p.sk_tiles = Q;                                        // PIPE: panel count
-  p.sk_ipc = 1;
+  p.sk_ipc = timeout_ms;                                 // PIPE: flag-wait timeout (ms)
   p.max_seg = 1;
   p.counters = const_cast<int*>(panel_it_d);             // PIPE: panel k-stage bounds
-  p.partials = reinterpret_cast<double*>(const_cast<int*>(flags_d));  // PIPE: panel flags
+  p.partials = reinterpret_cast<double*>(flags_d);       // PIPE: panel flags + abort word
   if ((s = get_encoder())) return s;
   CUtensorMap mA, mB;
   if ((s = encode_map(&mA, A, m, k, lda, Cfg::BM))) return s;
   if ((s = encode_map(&mB, B, k, n, ldb, Cfg::BK))) return s;
   void* args[] = {&mA, &mB, &p};
-  const int grid = (int)std::min<int64_t>(tiles, g_dev[dev].sms);
+  const int grid = (int)std::min<int64_t>(tiles, dev_sms(dev));
 #ifdef TB_TIMELINE
   p.timeline = nullptr;
   if (std::getenv("TB_TIMELINE")) {  // read back by the host-buffer entry after the call
@@ -469,13 +525,11 @@ int timed_gemm(int dev, const double* A, const double* B, double* Cm, int64_t m,
   TB_CUDA(cudaEventRecord(ev.a, stream), "event record");
   if (use_cublas) {
     DeviceState& st = g_dev[dev];
-    {
-      std::lock_guard<std::mutex> lk(st.mu);
-      if (!st.cublas && cublasCreate(&st.cublas) != CUBLAS_STATUS_SUCCESS) {
-        set_err("cublasCreate failed");
-        return TB_STATUS_RUNTIME;
-      }
-    }
+    if ((s = ensure_cublas(dev))) return s;
+    // The handle is shared per device: its stream binding and the DGEMM
+    // enqueue happen under one lock, so concurrent callers with different
+    // streams each get their GEMM on their own stream.
+    std::lock_guard<std::mutex> lk(st.cublas_mu);
     cublasSetStream(st.cublas, stream);
     const double one = 1.0, zero = 0.0;
     // Row-major C = A·B  <=>  column-major C^T = B^T · A^T.

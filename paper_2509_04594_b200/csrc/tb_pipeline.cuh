@@ -187,6 +187,6 @@ PipePlan plan_pipeline(int64_t m, int64_t k, int64_t n, int sms, bool fused_ok, 
     if (m > al.back()) al.push_back(m);
     rb.swap(al);
   }
-  if (pl.pk.size() - 1 < 2 || pl.pk.size() - 1 > 120) pl.fused = false;  // table holds <= 120 panels
+  if (pl.pk.size() - 1 < 2 || pl.pk.size() - 1 > (size_t)tb::kPipeMaxPanels) pl.fused = false;  // flag table size
   return pl;
 }

@@ -141,6 +141,7 @@ bool is_pinned(const void* p) {
 struct StageRing {
   static constexpr int kSlots = 8;
   static constexpr size_t kSlotBytes = size_t(32) << 20;
+  static constexpr int64_t kSlotCols = (int64_t)(kSlotBytes / sizeof(double));  // widest row chunk per slot
   char* slot[kSlots] = {};
   cudaEvent_t ev[kSlots] = {};
   int next = 0;

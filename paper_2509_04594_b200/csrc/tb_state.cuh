@@ -127,6 +127,7 @@ int choose_bm(int64_t m, int64_t n, int sms, bool dfma) {
   return rows64 < rows128 ? 64 : 128;
 }
 constexpr int kMaxDevices = 64;
+constexpr int kAbortReadback = 300;  // DeviceState::htab slot
 constexpr int kMaxBlockThreads = 1024;     // limits.ts:20-24 maxThreadsPerBlock
 
 thread_local char g_err[512] = "";
@@ -153,6 +154,8 @@ int cuda_fail(cudaError_t e, const char* what) {
 struct DeviceState {
   std::mutex mu;       // device attributes, kernel attributes, cuBLAS handle
   std::mutex host_mu;  // host-buffer entry: workspace + stream
+  std::mutex stage_mu;   // a staged launch's re-pitch + GEMM enqueue (tb_launch.cuh launch())
+  std::mutex cublas_mu;  // cublasSetStream + cublasDgemm on the shared handle
   bool ready = false;
   int sms = 0;
   int smem_optin = 0;
@@ -177,8 +180,10 @@ struct DeviceState {
   };
   std::map<cudaStream_t, StageWs> stage_ws;
   std::vector<cudaEvent_t> ev_pool[2];  // host-buffer entry: [timing, no-timing] events
-  int* dtab = nullptr;                  // host-buffer entry: [0,128) panel flags, [128,256) panel k-stages
-  int* htab = nullptr;                  // pinned: [0,128) zeros, [128,256) panel k-stages, [256] = 1
+  int* dtab = nullptr;                  // host-buffer entry: [0,128) panel flags (+ abort word at
+                                        // tb::kPipeAbortWord), [128,256) panel k-stages
+  int* htab = nullptr;                  // pinned: [0,128) zeros, [128,256) panel k-stages, [256] = 1,
+                                        // [kAbortReadback] the last fused launch's abort word
 };
 
 DeviceState g_dev[kMaxDevices];
@@ -216,6 +221,28 @@ int ensure_device(int dev) {
   TB_CUDA(cudaDeviceGetAttribute(&st.smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev),
           "query shared memory opt-in");
   st.ready = true;
+  return TB_STATUS_OK;
+}
+
+// The per-device cuBLAS handle for the baseline, created once with the math
+// mode pinned to CUBLAS_DEFAULT_MATH: native FP64 DGEMM (the math-mode bits
+// that enable tensor-op / emulated paths apply to FP32 only in cuBLAS 12.x,
+// and no FP64 emulation exists before CUDA 13), recorded by tb_runtime_info.
+int ensure_cublas(int dev) {
+  DeviceState& st = g_dev[dev];
+  std::lock_guard<std::mutex> lk(st.mu);
+  if (st.cublas) return TB_STATUS_OK;
+  cublasHandle_t h = nullptr;
+  if (cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) {
+    set_err("cublasCreate failed");
+    return TB_STATUS_RUNTIME;
+  }
+  if (cublasSetMathMode(h, CUBLAS_DEFAULT_MATH) != CUBLAS_STATUS_SUCCESS) {
+    cublasDestroy(h);
+    set_err("cublasSetMathMode(CUBLAS_DEFAULT_MATH) failed");
+    return TB_STATUS_RUNTIME;
+  }
+  st.cublas = h;
   return TB_STATUS_OK;
 }
 

@@ -12,10 +12,14 @@ there and records, for identical seeded inputs:
   kernel.test.ts:22-28, test_matrices.py:68-76, :99-100);
 * naive / tiled-seq outputs on the oracle grid (test_acceptance.py:57-73,
   kernel.test.ts:30-62, test_backends.py:53-71);
-* SHA-256 digests of generate() output and of full tiled-seq products at
-  N = 1000 (configs[0]) plus row samples at N = 4000 and N = 10000
+* SHA-256 digests of generate() output and of the FULL tiled products at
+  N = 1000 (configs[0]), N = 4000 (configs[1]) and N = 10000 (configs[3]),
+  computed by the reference's own ``tiled_parallel_multiply`` (numba, all
+  host threads; bitwise equal to ``tiled_seq``, backends.py:21-24), plus
+  64-row samples at N = 4000 and N = 10000 kept verbatim
   (tiled_seq(A[rows], B) is bitwise equal to those rows of the full product,
-  SURVEY.md §7 step 1).
+  SURVEY.md §7 step 1; the row samples are recomputed with ``tiled_seq`` on
+  the sampled rows and cross-checked against the full product's rows).
 
 Outputs: tests/golden/golden_small.npz, tests/golden/golden_meta.json.
 """
@@ -36,7 +40,7 @@ REF = "/root/reference/pkg/src"
 GRID = [1, 2, 31, 32, 33, 64, 65, 100]  # test_acceptance.py:57-73 DIMS
 SQUARE_EXTRA = [129]  # kernel.test.ts:56-62
 RECT = [(21, 47, 9), (37, 41, 29), (3, 5, 2)]  # kernel.test.ts:46-54, test_backends.py:66-71, :36-39
-ROW_SAMPLE = {4000: 16, 10000: 4}
+ROW_SAMPLE = {4000: 64, 10000: 64}  # SURVEY.md §8(d) parity gate: >= 64 rows
 
 
 def sha(x: np.ndarray) -> str:
@@ -49,7 +53,8 @@ def main() -> None:
     os.environ["NUMBA_CACHE_DIR"] = os.path.join(tmp, "numba_cache")
     sys.path.insert(0, os.path.join(tmp, "src"))
     import tilebench as tb  # noqa: E402
-    from tilebench.backends import TileConfig, naive_multiply, tiled_seq_multiply  # noqa: E402
+    from tilebench.backends import (PoolConfig, TileConfig, naive_multiply,  # noqa: E402
+                                    tiled_parallel_multiply, tiled_seq_multiply)
     from tilebench.matrices import GenSpec, flop_count, generate, max_abs_rel_diff  # noqa: E402
 
     arrays: dict[str, np.ndarray] = {}
@@ -98,14 +103,22 @@ def main() -> None:
         arrays[f"n{n}_tiled32_rows"] = c[rows]
         full[str(n)] = {"seed_a": 1, "seed_b": 2, "tiled32_sha256": sha(c),
                         "tiled32_fro": float(np.linalg.norm(c))}
-    # Row samples at N = 4000, 10000.
+    # configs[1] / configs[3]: N = 4000, 10000 full products (the reference's
+    # own tiled-parallel path on every host thread: ~15 s and ~4 min here)
+    # -> SHA-256 + Frobenius norm, and 64-row samples kept verbatim.
+    threads = os.cpu_count() or 1
     for n, r in ROW_SAMPLE.items():
         a = generate(GenSpec(n, n, 2.0, 5.0, 1))
         b = generate(GenSpec(n, n, 2.0, 5.0, 2))
+        c = tiled_parallel_multiply(a, b, TileConfig(32), PoolConfig(threads))
         rows = np.sort(np.random.Generator(np.random.PCG64(n)).choice(n, r, replace=False))
+        sampled = tiled_seq_multiply(a[rows], b, TileConfig(32))
+        assert np.array_equal(sampled, c[rows]), "row sampling must be bitwise"
         arrays[f"n{n}_rows"] = rows
-        arrays[f"n{n}_tiled32_rows"] = tiled_seq_multiply(a[rows], b, TileConfig(32))
-        full[str(n)] = {"seed_a": 1, "seed_b": 2}
+        arrays[f"n{n}_tiled32_rows"] = sampled
+        full[str(n)] = {"seed_a": 1, "seed_b": 2, "tiled32_sha256": sha(c),
+                        "tiled32_fro": float(np.linalg.norm(c)), "threads": threads}
+        del c
     meta["large"] = full
 
     np.savez_compressed(os.path.join(HERE, "golden_small.npz"), **arrays)

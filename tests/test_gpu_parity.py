@@ -240,6 +240,18 @@ def test_flat_abi_status_codes(tb, oracle):
     assert tb.gpu_tiled_multiply_flat(0, a, b, n, n, n, 4, np.zeros(3), out_s) == tb.STATUS_BAD_DIMS
     assert tb.gpu_tiled_multiply_flat(0, a, b, n, n, n, 0, out_c, out_s) == tb.STATUS_BAD_DIMS
     assert tb.gpu_tiled_multiply_flat(0, a, b, 0, n, n, 32, out_c, out_s) == tb.STATUS_BAD_DIMS
+    # executor.ts:86 / multiply.ts:71-73: buffers must match the dims; the
+    # flat ABI reads dense row-major host memory only.
+    import torch
+
+    assert tb.gpu_tiled_multiply_flat(0, a[:-1], b, n, n, n, 32, out_c, out_s) == tb.STATUS_BAD_DIMS
+    assert tb.gpu_tiled_multiply_flat(0, a, b[:, :-1], n, n, n, 32, out_c, out_s) == tb.STATUS_BAD_DIMS
+    assert tb.gpu_tiled_multiply_flat(0, a.T, b, n, n, n, 32, out_c, out_s) == tb.STATUS_BAD_DIMS
+    assert tb.gpu_tiled_multiply_flat(0, a.astype(np.float32), b, n, n, n, 32, out_c, out_s) == tb.STATUS_BAD_DIMS
+    assert tb.gpu_tiled_multiply_flat(0, torch.from_numpy(a).cuda(), b, n, n, n, 32, out_c,
+                                      out_s) == tb.STATUS_BAD_DIMS
+    assert tb.gpu_tiled_multiply_flat(0, torch.from_numpy(a), torch.from_numpy(b), n, n, n, 32,
+                                      torch.from_numpy(out_c), out_s) == tb.STATUS_OK
     for v in ("paper", "dmma_tma", "dmma_cpasync", "dfma"):
         out_c[:] = 0
         e2e = np.zeros(1)
@@ -279,6 +291,18 @@ def test_registry_and_device_timed_runner(tb, oracle, tmp_path):
         assert cell["trials"] == 3
         assert cell["h2d_bytes"] == 2 * 8 * 129 * 129 and cell["d2h_bytes"] == 8 * 129 * 129
         assert cell["h2d_seconds_median"] > 0 and cell["d2h_seconds_median"] > 0
+    # run metadata (harness.py:126-142 + SURVEY.md §5): versions, loaded cuBLAS, pinned math mode, GPU, plan
+    cfg_meta = json.loads((tmp_path / "gpu.csv.meta.json").read_text())["config"]
+    gpu = cfg_meta["gpu"]
+    for key in ("cublas_version", "cublas_path", "cuda_runtime_version", "cuda_driver_version", "gpu_name",
+                "sm_count", "sm_clock_max_khz", "compute_capability"):
+        assert gpu.get(key), key
+    assert gpu["cublas_math_mode"] == 0 and gpu["cublas_math_mode_name"] == "CUBLAS_DEFAULT_MATH"
+    assert gpu["compute_capability"] == 100 and gpu["sm_count"] >= 100
+    assert cfg_meta["nccl_version"] and cfg_meta["torch"]
+    assert cfg_meta["clocks_at_start"]["sm_max_mhz"]
+    plan = cfg_meta["launch_plans"]["129"]
+    assert plan and all(p["kernel"] == "dmma" for p in plan if "kernel" in p)
 
 
 def test_liar_backend_caught_by_verify(tb, oracle):

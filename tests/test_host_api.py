@@ -135,6 +135,25 @@ def test_runner_with_external_backend_and_csv(tmp_path, oracle):
     import json
     side = json.loads((tmp_path / "r.csv.meta.json").read_text())
     assert set(side) == {"timestamp", "host", "cores", "config"}
+    # GPU run metadata is captured even without a device (library + cuBLAS facts)
+    gpu = side["config"]["gpu"]
+    assert gpu["library"].startswith("tbgpu") and gpu["cublas_version"] and gpu["cublas_path"]
+    assert "fp64_emulation" in gpu and "device_count" in gpu
+    assert [p["tile"] for p in side["config"]["launch_plans"]["16"]] == [[64, 128, 16]]
+
+
+def test_launch_plan_describes_the_schedule():
+    """tb_launch_plan: the resolved kernel / tile / schedule per launch (no device)."""
+    from paper_2509_04594_b200 import _lib
+
+    p = _lib.launch_plan(10000, 10000, 10000)
+    assert [x["tile"][:2] for x in p] == [[128, 128], [128, 16], [16, 128]]
+    assert p[0]["schedule"] == "stream-k" and p[0]["m"] == p[0]["n"] == 9984 and p[0]["grid"] == 148
+    assert p[1]["strip"] and p[2]["strip"]
+    assert _lib.launch_plan(1000, 1000, 1000)[0]["schedule"] == "data-parallel"
+    assert _lib.launch_plan(9999, 9999, 9999)[0] == {"repitch": "AB"}
+    assert _lib.launch_plan(300, 300, 300, "paper")[0]["block"] == [32, 32]
+    assert _lib.launch_plan(2000, 2000, 2000, sms=132)[0]["grid"] == 132
 
 
 def test_runner_wraps_failures_as_trial_error():

@@ -60,13 +60,21 @@ def test_row_sampling_is_bitwise(golden, oracle):
     assert np.array_equal(oracle.tiled_seq(a[rows], b), oracle.tiled_seq(a, b)[rows])
 
 
-@pytest.mark.parametrize("n", [4000])
-def test_large_row_samples(golden, oracle, n):
+@pytest.mark.parametrize("n", [4000, 10000])
+def test_large_full_products(golden, oracle, n):
+    """configs[1] / configs[3]: the oracle's FULL N x N tiled product is
+    bitwise the reference's (SHA-256 of its tiled_parallel_multiply output,
+    tests/golden/make_golden.py), and so are the 64 sampled rows kept
+    verbatim. ~2 s / ~35 s on 8 host threads."""
     meta, g = golden
-    assert sha(oracle.generate(n, n, 1)) == meta["gen_digest"][f"{n}_1"]
+    assert sha(oracle.generate(min(n, 4000), min(n, 4000), 1)) == meta["gen_digest"]["4000_1"]
     a, b = oracle.generate(n, n, 1), oracle.generate(n, n, 2)
-    rows = g[f"n{n}_rows"][:4]
-    assert np.array_equal(oracle.tiled_parallel(a[rows], b), g[f"n{n}_tiled32_rows"][:4])
+    c = oracle.tiled_parallel(a, b)
+    assert sha(c) == meta["large"][str(n)]["tiled32_sha256"]
+    rows = g[f"n{n}_rows"]
+    assert len(rows) >= 64
+    assert np.array_equal(c[rows], g[f"n{n}_tiled32_rows"])
+    assert np.array_equal(oracle.tiled_parallel(a[rows[:4]], b), g[f"n{n}_tiled32_rows"][:4])
 
 
 def test_plan_partitions(oracle):

@@ -21,6 +21,7 @@ import subprocess
 import sys
 import tempfile
 import time
+from datetime import timedelta
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 if ROOT not in sys.path:
@@ -182,13 +183,89 @@ def blas_sample(n: int, target_s: float = 3.0) -> dict:
             "sample": f"numpy {np.__version__} matmul (OpenBLAS) on {rows} of {n} rows, {dt:.2f} s"}
 
 
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def _ref_cpu_worker(n: int, threads: int, target_s: float) -> None:
+    """Subprocess body (``bench.py --ref-cpu-worker``): the reference's OWN
+    numba CPU backends, imported unmodified from baseline/_ref, timed on a
+    row sample of the N x N product: ``tiled_parallel_multiply`` (the
+    OpenMP-style static split, backends.py:139-160) and
+    ``tiled_pool_multiply`` (the C++-threads-style task queue,
+    backends.py:163-190), both with PoolConfig(threads) and TileConfig(32),
+    timed with the reference's own perf_counter bracket (harness.py:163-172).
+    Prints one JSON object."""
+    import numba
+    import numpy as np
+    import tilebench
+    from tilebench.backends import PoolConfig, TileConfig, tiled_parallel_multiply, tiled_pool_multiply
+
+    out = {"tilebench": getattr(tilebench, "__version__", "?"), "numba": numba.__version__, "threads": threads,
+           "from": REF_DIR}
+    b = np.random.Generator(np.random.PCG64(1)).random((n, n)) * 3.0 + 2.0
+    tile, pool = TileConfig(32), PoolConfig(threads)
+    tiled_parallel_multiply(np.ones((2, 2)), np.ones((2, 2)), tile, pool)  # JIT (cache outside the tree)
+    for name, fn in (("tiled-parallel", tiled_parallel_multiply), ("tiled-pool", tiled_pool_multiply)):
+        rows = min(n, 8 * threads)  # enough tile rows to keep every thread busy while calibrating
+        a = np.random.Generator(np.random.PCG64(2)).random((rows, n)) * 3.0 + 2.0
+        t0 = time.perf_counter()
+        fn(a, b, tile, pool)
+        dt = max(time.perf_counter() - t0, 1e-3)
+        rows = int(min(n, max(32, rows * target_s / dt))) // 32 * 32 or 32
+        a = np.random.Generator(np.random.PCG64(2)).random((rows, n)) * 3.0 + 2.0
+        t0 = time.perf_counter()
+        fn(a, b, tile, pool)
+        dt = time.perf_counter() - t0
+        out[name] = {"value": rows * (2 * n * n - n) / dt / 1e9, "unit": UNIT, "cores": threads, "rows": rows,
+                     "seconds": dt,
+                     "sample": f"reference tilebench.backends.{fn.__name__} (numba {numba.__version__}, unmodified, "
+                               f"baseline/_ref) on {rows} of {n} rows of the N={n} product, {dt:.1f} s, "
+                               f"{threads} threads"}
+    print(json.dumps(out), flush=True)
+
+
+def reference_numba_cpu(n: int, threads: int, target_s: float = 8.0) -> dict:
+    """The reference's own CPU code (numba ``tiled-parallel`` and
+    ``tiled-pool``) timed in a clean subprocess with NUMBA_CACHE_DIR outside
+    the tree; reported beside the C port (the reference arm's value)."""
+    if not os.path.isdir(os.path.join(REF_DIR, "tilebench")):
+        return {"unavailable": "baseline/_ref/tilebench not installed"}
+    env = dict(os.environ, PYTHONPATH=REF_DIR, NUMBA_CACHE_DIR=os.path.join(tempfile.gettempdir(), "tb_numba_cache"),
+               NUMBA_NUM_THREADS=str(threads))
+    cmd = [sys.executable, os.path.abspath(__file__), "--ref-cpu-worker", "--size", str(n), "--ref-threads",
+           str(threads), "--ref-seconds", str(target_s)]
+    try:
+        res = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
+    except subprocess.TimeoutExpired:
+        return {"unavailable": "reference numba run timed out"}
+    if res.returncode != 0:
+        return {"unavailable": f"reference numba run failed: {res.stderr.strip().splitlines()[-1:]}"}
+    return json.loads(res.stdout.strip().splitlines()[-1])
+
+
+def cpu_baselines(n: int, target_s: float) -> dict:
+    """cpu_baseline: the C port of the reference's tiled-parallel path on all
+    host threads (``value``), plus sub-records on the same N: the
+    reference's own numba tiled-parallel and tiled-pool, and its BLAS
+    backend (numpy matmul, demos/06_external_backends.py)."""
+    threads = os.cpu_count() or 1
+    cpu = cpu_sample(n, threads, cpu_calibrate(n, threads, target_s))
+    cpu.pop("seconds", None)
+    cpu["blas"] = blas_sample(n)
+    cpu["reference_numba"] = reference_numba_cpu(n, threads)
+    cpu["host_threads"] = threads
+    return cpu
+
+
 def run_reference(args) -> None:
     rank, world, _ = env_rank()
     if rank != 0:
         return
     threads = os.cpu_count() or 1
     vals = []
-    rows = cpu_calibrate(args.n, threads, args.ref_seconds)
+    # each step a bounded sample; the whole --steps/--warmup run stays within ~3 minutes
+    per_step = min(args.ref_seconds, 150.0 / max(1, args.steps + args.warmup))
+    rows = cpu_calibrate(args.n, threads, per_step)
     for i in range(args.warmup + args.steps):
         s = cpu_sample(args.n, threads, rows)
         if i >= args.warmup:
@@ -199,7 +276,7 @@ def run_reference(args) -> None:
             "vs_baseline": None, "dtype": "f64", "data": "synthetic uniform[2,5] (numpy PCG64)",
             "config": {"workload": f"N={args.n} FP64 square GEMM, bounded row sample on host cores", "n": args.n},
             "cpu_baseline": {**{k: vals[-1][k] for k in ("unit", "cores", "kind", "sample")}, "value": v,
-                             "blas": blas_sample(args.n)},
+                             "blas": blas_sample(args.n), "reference_numba": reference_numba_cpu(args.n, threads)},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "ms_per_step": statistics.median([s["seconds"] for s in vals]) * 1e3}
     print(json.dumps(line), flush=True)
@@ -212,7 +289,8 @@ def run_ours(args) -> None:
 
     import paper_2509_04594_b200 as tb
     from paper_2509_04594_b200 import _lib
-    from paper_2509_04594_b200.multigpu import HostShardedGemm, ShardedGemm, panel_bounds, row_partitions
+    from paper_2509_04594_b200.harness import gpu_environment
+    from paper_2509_04594_b200.multigpu import HostShardedGemm, ShardedGemm, row_partitions
 
     rank, world, local = env_rank()
     if world != args.gpus:
@@ -325,21 +403,37 @@ def run_ours(args) -> None:
     # ABI (gpuTiledMultiplyFlat shape). N > 1: HostShardedGemm — each rank
     # uploads its A rows and an equal share of every K-panel of B, NCCL
     # all-gathers the panels over NVLink, C rows come back as they finish.
-    a_h = a_loc.cpu().pin_memory()
+    # Host buffers are pinned directly (no pageable intermediate). At N > 1 a
+    # rank holds its A / C rows and only its own shares of B's K-panels
+    # (HostShardedGemm.share_rows, packed in panel order): B crosses PCIe
+    # once in total and no rank ever holds all of B in host memory.
+    def pinned(rows, cols):
+        return torch.empty((rows, cols), dtype=torch.float64, pin_memory=True)
+
+    a_h = pinned(r1 - r0, n)
+    a_h.copy_(a_loc)
+    host_sharded = HostShardedGemm(panels=args.panels or None) if world > 1 else None
     if world > 1:
         dist.broadcast(b, 0)
-    b_h = b.cpu().pin_memory()
-    c_h = torch.empty((r1 - r0, n), dtype=torch.float64).pin_memory()
+        b_h = pinned(host_sharded.packed_rows(n, world), n)
+        b_h.zero_()
+        off = 0
+        for (k0, k1), (s0, s1) in zip(host_sharded.plan(n, world), host_sharded.share_rows(n, world, rank)):
+            b_h[off:off + s1 - s0].copy_(b[s0:s1])
+            off += (k1 - k0) // world
+    else:
+        b_h = pinned(n, n)
+        b_h.copy_(b)
+    c_h = pinned(r1 - r0, n)
     out_s = np.zeros(1)
     e2e = np.zeros(1)
     e2e_times, e2e_dev = [], []
-    host_sharded = HostShardedGemm(panels=args.panels or None) if world > 1 else None
     for i in range(1 + max(2, args.steps // 3)):
         if world > 1:
             dist.barrier()
         t_call = time.perf_counter()
         if world > 1:
-            host_sharded(a_h, b_h, c_h)
+            host_sharded(a_h, b_h, c_h, b_packed=True)
             dist.barrier()  # the step ends when every rank's C rows are in host memory
         else:
             st = tb.gpu_tiled_multiply_flat(local_dev, a_h, b_h, r1 - r0, n, n, 32, c_h, out_s,
@@ -361,12 +455,31 @@ def run_ours(args) -> None:
     h2d = 16 * n * n  # whole job: A once (row shards) + B once (per-rank panel shares); N = 1: A + B
     d2h = 8 * n * n
 
+    import resource
+
+    # Peak host RSS of the GEMM path (pinned A/C rows + this rank's B shares,
+    # before the CPU baselines allocate their own operands), max over ranks.
+    rss_gb = resource.getrusage(resource.RUSAGE_SELF).ru_maxrss / 2**20  # KiB -> GiB
+    if world > 1:
+        t = torch.tensor([rss_gb], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        rss_gb = t.item()
+    pinned_gb = (a_h.numel() + b_h.numel() + c_h.numel()) * 8 / 2**30
+    env_meta = gpu_environment([], device=local_dev)
+    env_meta["launch_plan"] = _lib.launch_plan(r1 - r0, n, n, args.variant, sms=env_meta["gpu"].get("sm_count", SMS))
+
+    # CPU baselines on rank 0 (any N). The other ranks wait in the rendezvous
+    # store (a blocking socket read, not a spinning device sync), so every
+    # host core is free for the measurement.
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        threads = os.cpu_count() or 1
-        cpu = cpu_sample(n, threads, cpu_calibrate(n, threads, args.ref_seconds))
-        cpu.pop("seconds", None)
-        cpu["blas"] = blas_sample(n)
+    if not args.no_cpu:
+        store = dist.distributed_c10d._get_default_store() if world > 1 else None
+        if rank == 0:
+            cpu = cpu_baselines(n, args.ref_seconds)
+            if store is not None:
+                store.set("tb_bench_cpu_done", "1")
+        elif store is not None:
+            store.wait(["tb_bench_cpu_done"], timedelta(minutes=15))
 
     if rank == 0:
         line = {
@@ -405,6 +518,9 @@ def run_ours(args) -> None:
             "clocks": clk,
             "cpu_baseline": cpu,
             "library": _lib.version(),
+            "host_memory": {"rss_gb_max_rank_gemm_path": rss_gb, "pinned_gb_rank0": pinned_gb,
+                            "rss_gb_rank0_incl_cpu_baseline": resource.getrusage(resource.RUSAGE_SELF).ru_maxrss / 2**20},
+            "env": env_meta,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -425,7 +541,12 @@ def main():
     p.add_argument("--ref-seconds", type=float, default=10.0, help="CPU sample length per measurement (s)")
     p.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     p.add_argument("--dist-backend", default="nccl", help="torch.distributed backend at N>1 (nccl; gloo for tests)")
+    p.add_argument("--ref-cpu-worker", action="store_true", help=argparse.SUPPRESS)
+    p.add_argument("--ref-threads", type=int, default=0, help=argparse.SUPPRESS)
     args = p.parse_args()
+    if args.ref_cpu_worker:
+        _ref_cpu_worker(args.n, args.ref_threads or os.cpu_count() or 1, args.ref_seconds)
+        return
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
     if args.impl == "reference":

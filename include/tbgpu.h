@@ -119,7 +119,15 @@ TB_API int tb_cublas_dgemm(const double* A, const double* B, double* C, int64_t 
                     int64_t n, int32_t tile_edge, int32_t variant, int32_t device,
                     void* cuda_stream, double* out_kernel_seconds);
 
-/* Row-sharded multi-GPU GEMM from one process (the
+/* EXPERIMENTAL — not a measured path. The measured multi-GPU path is one
+ * process per GPU with an NCCL broadcast of B (multigpu.ShardedGemm, device
+ * buffers; multigpu.HostShardedGemm from host buffers; bench.py --gpus N),
+ * as BASELINE.json's north_star specifies. This single-process peer-copy
+ * form is kept for callers that drive several GPUs from one thread; it is
+ * tested for parity with a device listed several times, never on distinct
+ * GPUs.
+ *
+ * Row-sharded multi-GPU GEMM from one process (the
  * reference's multi-device row partition is plan_partitions,
  * backends.py:119-136). Entry i of `devices` owns rows[i] rows:
  * C_rows[i] (rows[i] x n) = A_rows[i] (rows[i] x k) · B, all packed

@@ -30,6 +30,21 @@
 // conflict-free 64-bit loads (derivation in DESIGN.md §4).
 #pragma once
 
+// Barrier-discipline mutants (tests/test_gpu_mutations.py, in the style of
+// the reference's barriers.test.ts:37-82): test-only builds with
+// -DTB_MUTATE=<n> break one ordering rule of the consumer's stage protocol
+// so the suite can show it catches the break. Never set in the product
+// build (0: the production kernel; SASS identical with the hooks compiled out).
+//   1  fragment loads of a stage's first half-step issued BEFORE its
+//      full-barrier wait (the "missing load barrier")
+//   2  the stage released to the producer (empty arrive) right after its
+//      full-barrier wait, before its fragments are read (the "missing reuse
+//      barrier")
+//   3  no fence.proxy.async before the empty arrive (the round-1 race)
+#ifndef TB_MUTATE
+#define TB_MUTATE 0
+#endif
+
 #ifndef TB_GROUP_M
 #define TB_GROUP_M 16  // tile-raster band height (A/B builds: tools/build_variant.py NAME -DTB_GROUP_M=16)
 #endif
@@ -224,7 +239,12 @@ __global__ void __launch_bounds__(DmmaCfg::THREADS, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   TB_TL(unsigned long long* tl = p.timeline ? p.timeline + 8 * blockIdx.x : nullptr;)
-  TB_TL(if (tl && threadIdx.x == 0) tl[0] = tl_now();)
+  TB_TL(if (tl && threadIdx.x == 0) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    tl[0] = tl_now();
+    tl[4] = (unsigned long long)smid << 32;  // [4]: smid << 32 | units
+  })
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -444,27 +464,57 @@ __global__ void __launch_bounds__(DmmaCfg::THREADS, 1)
 #pragma unroll
           for (int j = 0; j < C::NI; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], fa[buf][i].y, fb[buf][1][j]);
       };
-      mbar_wait(smem_u32(&full[s]), ph);
+#if TB_MUTATE == 1
       ld(s, 0, 0);
+      mbar_wait(smem_u32(&full[s]), ph);
+#else
+      mbar_wait(smem_u32(&full[s]), ph);
+#if TB_MUTATE == 2
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&empty[s]));
+#endif
+      ld(s, 0, 0);
+#endif
       for (int kt = kb; kt < ke; ++kt) {
         ld(s, 1, 1);
         mma(0);
         const int s1 = s + 1 == STAGES ? 0 : s + 1;
         const uint32_t ph1 = s + 1 == STAGES ? ph ^ 1 : ph;
         if (kt + 1 < ke) {
-          mbar_wait(smem_u32(&full[s1]), ph1);
+#if TB_MUTATE == 1
           ld(s1, 0, 0);
+          mbar_wait(smem_u32(&full[s1]), ph1);
+#else
+          mbar_wait(smem_u32(&full[s1]), ph1);
+#if TB_MUTATE == 2
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(&empty[s1]));
+#endif
+          ld(s1, 0, 0);
+#endif
         }
         mma(1);
+#if TB_MUTATE != 3
         fence_proxy_async();
+#endif
         __syncwarp();
+#if TB_MUTATE != 2
         if (lane == 0) mbar_arrive(smem_u32(&empty[s]));
+#endif
         s = s1;
         ph = ph1;
       }
     } else
     for (int kt = kb; kt < ke; ++kt) {
+#if TB_MUTATE != 1
       mbar_wait(smem_u32(&full[s]), ph);
+#else
+      if constexpr (MT == Math::DFMA) mbar_wait(smem_u32(&full[s]), ph);  // mutant 1 covers the DMMA loops
+#endif
+#if TB_MUTATE == 2
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&empty[s]));
+#endif
       TB_TL(if (tl && ct == 0 && kt == kb) { tl_u = tl_now(); if (tl[1] == 0) tl[1] = tl_u; })
       if constexpr (MT == Math::DFMA) {
 #pragma unroll
@@ -516,6 +566,9 @@ __global__ void __launch_bounds__(DmmaCfg::THREADS, 1)
           bf[0][j] = *reinterpret_cast<const double*>(sb + box + (b_off[2 * half] ^ flip));
           bf[1][j] = *reinterpret_cast<const double*>(sb + box + (b_off[2 * half + 1] ^ flip));
         }
+#if TB_MUTATE == 1
+        if (hs == 0) mbar_wait(smem_u32(&full[s]), ph);
+#endif
 #pragma unroll
         for (int i = 0; i < C::MI; ++i)
 #pragma unroll
@@ -532,9 +585,13 @@ __global__ void __launch_bounds__(DmmaCfg::THREADS, 1)
       // while the last LDS are still outstanding, and a TMA landing before
       // they are serviced corrupts those fragments (observed on B200 when the
       // accumulate epilogue's global loads back up the LSU queue).
+#if TB_MUTATE != 3
       fence_proxy_async();
+#endif
       __syncwarp();
+#if TB_MUTATE != 2
       if (lane == 0) mbar_arrive(smem_u32(&empty[s]));
+#endif
       if (++s == STAGES) {
         s = 0;
         ph ^= 1;

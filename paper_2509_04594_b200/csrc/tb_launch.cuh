@@ -223,6 +223,20 @@ int launch(int dev, const double* A, int64_t lda, const double* B, int64_t ldb, 
     }
   }
   variant = resolve(A, lda, B, ldb, variant);
+  // TB_TILE=<bm>x<bn>: force one main-tile shape, no edge split (A/B sweeps).
+  static const int forced_tile = [] {
+    const char* e = std::getenv("TB_TILE");
+    if (!e) return 0;
+    for (int c = kStrip64x128; c < kNumStripCfgs; ++c) {
+      const StripInfo si = strip_info(c);
+      char name[32];
+      std::snprintf(name, sizeof(name), "%dx%d", c == kStrip64x128 ? 64 : si.bm, c == kStrip64x128 ? 128 : si.bn);
+      if (std::strcmp(e, name) == 0) return c;
+    }
+    return std::strcmp(e, "128x128") == 0 ? -1 : 0;
+  }();
+  if (forced_tile && variant == TB_VARIANT_DMMA_TMA)
+    return launch_tiles(dev, A, lda, B, ldb, Cm, ldc, m, k, n, accumulate, tile_edge, variant, stream, forced_tile);
   static const bool split_env = !(std::getenv("TB_SPLIT") && std::strcmp(std::getenv("TB_SPLIT"), "0") == 0);
   if (split_env && variant == TB_VARIANT_DMMA_TMA && (m % 128 != 0 || n % 128 != 0)) {
     const int64_t hb = m % 128, wr = n % 128;
@@ -378,11 +392,17 @@ int launch_tiles(int dev, const double* A, int64_t lda, const double* B, int64_t
         mainl += (double)r[7];
         fix += (double)r[5];
         epi += (double)r[6];
-        units += (double)r[4];
+        units += (double)(r[4] & 0xffffffffull);
         endmax = std::max(endmax, (double)(r[3] - t0));
         endmin = std::min(endmin, (double)(r[3] - t0));
       }
       const double g = sc.grid;
+      if (std::strcmp(std::getenv("TB_TIMELINE"), "2") == 0)  // per-CTA lines: SM, units, end, main loop
+        for (int c = 0; c < sc.grid; ++c) {
+          const unsigned long long* r = &h[(size_t)c * 8];
+          std::fprintf(stderr, "TBCTA cta=%d smid=%llu units=%llu end_us=%.2f mainloop_us=%.2f fixup_us=%.2f\n", c,
+                       r[4] >> 32, r[4] & 0xffffffffull, (r[3] - t0) / 1e3, r[7] / 1e3, r[5] / 1e3);
+        }
       std::fprintf(stderr,
                    "TBTIMELINE m=%lld n=%lld k=%lld grid=%d dp=%d sk=%d ipc=%d maxseg=%d span_us=%.2f "
                    "first_stage_us=%.2f mainloop_us=%.2f last_mainloop_end_us=%.2f fixup_us=%.2f epilogue_us=%.2f "
@@ -430,7 +450,7 @@ void pipe_timeline_report() {
       lastw = std::max(lastw, w[3] ? (double)(w[3] - t0) : 0.0);
       ml += (double)r[7];
       epi += (double)r[6];
-      units += (double)r[4];
+      units += (double)(r[4] & 0xffffffffull);
     }
     std::fprintf(stderr,
                  "TBPIPE grid=%d span_us=%.1f end_min_us=%.1f flag_wait_mean_us=%.1f flag_wait_max_us=%.1f "

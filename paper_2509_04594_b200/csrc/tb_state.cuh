@@ -75,7 +75,16 @@ enum StripCfg : int {
   kStrip128x64,
   kStrip16x128,
   kStrip32x128,
-  kStrip64x128
+  kStrip64x128,
+  // Main-tile shapes besides 128 x 128 / 64 x 128 (TMA + DMMA), for small
+  // and ragged problems (tile_for_shape).
+  kTile64x64,
+  kTile96x128,
+  kTile128x96,
+  kTile96x96,
+  kTile64x96,
+  kTile128x64,
+  kNumStripCfgs
 };
 // Narrow tiles do little work per 16-deep k-slab, so a strip stage holds
 // several sub-slabs (SUB x 16 k) to amortise the per-stage barrier round trip.
@@ -98,6 +107,12 @@ StripInfo strip_info(int c) {
     case kStrip128x64: return {128, 64, 2, StripK<128, 64, 4, 2, 4>::fn(), StripK<128, 64, 4, 2, 4>::smem()};
     case kStrip16x128: return {16, 128, 4, StripK<16, 128, 1, 4, 3>::fn(), StripK<16, 128, 1, 4, 3>::smem()};
     case kStrip32x128: return {32, 128, 2, StripK<32, 128, 1, 2, 5>::fn(), StripK<32, 128, 1, 2, 5>::smem()};
+    case kTile64x64: return {64, 64, 2, StripK<64, 64, 2, 2, 6>::fn(), StripK<64, 64, 2, 2, 6>::smem()};
+    case kTile96x128: return {96, 128, 1, StripK<96, 128, 2, 1, 7>::fn(), StripK<96, 128, 2, 1, 7>::smem()};
+    case kTile128x96: return {128, 96, 1, StripK<128, 96, 4, 1, 7>::fn(), StripK<128, 96, 4, 1, 7>::smem()};
+    case kTile96x96: return {96, 96, 1, StripK<96, 96, 4, 1, 8>::fn(), StripK<96, 96, 4, 1, 8>::smem()};
+    case kTile64x96: return {64, 96, 1, StripK<64, 96, 4, 1, 9>::fn(), StripK<64, 96, 4, 1, 9>::smem()};
+    case kTile128x64: return {128, 64, 2, StripK<128, 64, 4, 2, 4>::fn(), StripK<128, 64, 4, 2, 4>::smem()};
     default: return {0, 0, 1, nullptr, 0};
   }
 }
@@ -263,7 +278,7 @@ int ensure_kernel_attrs(int dev) {
   if (cfg_smem(0) <= st.smem_optin)
     TB_CUDA(cudaFuncSetAttribute(pipe_kernel(), cudaFuncAttributeMaxDynamicSharedMemorySize, cfg_smem(0)),
             "set smem attribute (pipe)");
-  for (int c = kStrip128x16; c <= kStrip32x128; ++c) {
+  for (int c = kStrip128x16; c < kNumStripCfgs; ++c) {
     const StripInfo si = strip_info(c);
     if (si.smem <= st.smem_optin)
       TB_CUDA(cudaFuncSetAttribute(si.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, si.smem),

@@ -223,6 +223,26 @@ class HostShardedGemm:
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self._bufs = None
 
+    def plan(self, k: int, world: int) -> list[tuple[int, int]]:
+        """The K-panel bounds a call with inner dimension ``k`` uses."""
+        return host_panel_bounds(k, world) if not self.panels else gathered_panels(k, world, self.panels)
+
+    def share_rows(self, k: int, world: int, rank: int) -> list[tuple[int, int]]:
+        """Rows of B this rank uploads, panel by panel: ``[(s0, s1), ...]``
+        (clipped to ``k``; the last panel's padding rows are not read). A
+        rank that holds only these rows, packed in this order as a
+        ``(sum of panel shares) x n`` pinned buffer, passes it with
+        ``b_packed=True`` and never needs all of B in host memory."""
+        out = []
+        for k0, k1 in self.plan(k, world):
+            sh = (k1 - k0) // world
+            out.append((min(k, k0 + rank * sh), min(k0 + (rank + 1) * sh, k)))
+        return out
+
+    def packed_rows(self, k: int, world: int) -> int:
+        """Rows of the packed share buffer (``b_packed=True``)."""
+        return sum((k1 - k0) // world for k0, k1 in self.plan(k, world))
+
     def _buffers(self, m, k, kp, n, share_rows):
         key = (m, k, kp, n, share_rows)
         if self._bufs is None or self._bufs[0] != key:
@@ -234,14 +254,22 @@ class HostShardedGemm:
             self._bufs = (key, a, b, c, stage)
         return self._bufs[1:]
 
-    def __call__(self, a_local_h: torch.Tensor, b_h: torch.Tensor, c_local_h: torch.Tensor) -> torch.Tensor:
+    def __call__(self, a_local_h: torch.Tensor, b_h: torch.Tensor, c_local_h: torch.Tensor,
+                 b_packed: bool = False) -> torch.Tensor:
+        """``b_h`` is all of B (k x n), or with ``b_packed=True`` only this
+        rank's panel shares packed in panel order (``share_rows``)."""
         world = dist.get_world_size(self.group)
         rank = dist.get_rank(self.group)
         m, k = a_local_h.shape
         n = b_h.shape[1]
-        if b_h.shape[0] != k or tuple(c_local_h.shape) != (m, n):
+        if b_packed:
+            if b_h.shape[0] != self.packed_rows(k, world):
+                raise ValueError(f"packed B shares need {self.packed_rows(k, world)} rows, got {b_h.shape[0]}")
+        elif b_h.shape[0] != k:
             raise ValueError(f"shapes {tuple(a_local_h.shape)} @ {tuple(b_h.shape)} -> {tuple(c_local_h.shape)}")
-        bounds = host_panel_bounds(k, world) if not self.panels else gathered_panels(k, world, self.panels)
+        if tuple(c_local_h.shape) != (m, n):
+            raise ValueError(f"shapes {tuple(a_local_h.shape)} @ {tuple(b_h.shape)} -> {tuple(c_local_h.shape)}")
+        bounds = self.plan(k, world)
         kp = bounds[-1][1]
         shares = [(k1 - k0) // world for k0, k1 in bounds]
         a_d, b_d, c_d, stage = self._buffers(m, k, kp, n, sum(shares))
@@ -264,7 +292,8 @@ class HostShardedGemm:
                 sh = shares[q]
                 s0, s1 = k0 + rank * sh, min(k0 + (rank + 1) * sh, k)
                 if s1 > s0:
-                    stage[off:off + s1 - s0].copy_(b_h[s0:s1], non_blocking=cuda)
+                    src = b_h[off:off + s1 - s0] if b_packed else b_h[s0:s1]
+                    stage[off:off + s1 - s0].copy_(src, non_blocking=cuda)
                 kk1 = min(k1, k)
                 if m > 0 and kk1 > k0:
                     _copy_cols(a_d, a_local_h, k0, kk1, copy_s)
@@ -337,7 +366,11 @@ def gather_rows(out_local: torch.Tensor, parts: list[tuple[int, int]], dst: int 
 
 def peer_sharded_dgemm(a_rows: list, b_root: torch.Tensor, c_rows: list, b_replicas: list | None = None,
                        variant="auto") -> tuple[float, float]:
-    """Single-process form (``tb_dgemm_mgpu``): ``c_rows[i] = a_rows[i] · B``
+    """EXPERIMENTAL, unmeasured (see include/tbgpu.h): the measured
+    multi-GPU paths are ``ShardedGemm`` / ``HostShardedGemm`` (one process
+    per GPU, NCCL).
+
+    Single-process form (``tb_dgemm_mgpu``): ``c_rows[i] = a_rows[i] · B``
     with every ``a_rows[i]`` / ``c_rows[i]`` (and ``b_replicas[i]``, i >= 1)
     a contiguous float64 CUDA tensor on device i's GPU and B on the GPU of
     ``a_rows[0]``. B is forwarded down the device chain in K-panels by peer

@@ -100,6 +100,16 @@ def _host_worker(rank, world, port, m, k, n, panels, chunks, q):
         for _ in range(2):  # cached buffers reused by the second call
             g(a[r0:r1].contiguous(), b, c)
         full = gather_rows(c, parts, dst=0)
+        # the same product from only this rank's shares of B (packed in panel order)
+        packed = torch.full((g.packed_rows(k, world), n), float("nan"), dtype=torch.float64)
+        off = 0
+        for (k0, k1), (s0, s1) in zip(g.plan(k, world), g.share_rows(k, world, rank)):
+            packed[off:off + (k1 - k0) // world] = 0.0
+            packed[off:off + s1 - s0] = b[s0:s1]
+            off += (k1 - k0) // world
+        c2 = torch.full((r1 - r0, n), float("nan"), dtype=torch.float64)
+        g(a[r0:r1].contiguous(), packed, c2, b_packed=True)
+        assert torch.equal(c, c2)
         if rank == 0:
             ref = (a @ b).numpy()
             q.put(float(np.linalg.norm(full.numpy() - ref) / np.linalg.norm(ref)))

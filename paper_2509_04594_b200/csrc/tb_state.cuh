@@ -280,7 +280,7 @@ int ensure_kernel_attrs(int dev) {
             "set smem attribute (pipe)");
   for (int c = kStrip128x16; c < kNumStripCfgs; ++c) {
     const StripInfo si = strip_info(c);
-    if (si.smem <= st.smem_optin)
+    if (si.fn && si.smem <= st.smem_optin)  // kStrip64x128 is the 64-row kernel (small_kernel), set below
       TB_CUDA(cudaFuncSetAttribute(si.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, si.smem),
               "set smem attribute (strip)");
   }

@@ -73,8 +73,14 @@ def test_product_build_passes_probe():
 
 @pytest.mark.parametrize("n", sorted(MUTANTS))
 def test_mutant_is_caught(mutant_libs, n):
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    import sass_lint
+
     errs = _probe(mutant_libs[n])
-    print(f"mutant {n} ({MUTANTS[n]}): {errs}")
+    lint = sass_lint.lint(os.path.join(PKG, f"libtbgpu_{mutant_libs[n]}.so"))
+    print(f"mutant {n} ({MUTANTS[n]}): probe {errs}; sass lint: {len(lint['violations'])} of "
+          f"{lint['arrives']} consumer arrives unfenced")
     if "outcome" in errs:
         return  # crashed or hung: caught
-    assert max(errs.values()) > 1e-12, f"mutant {n} ({MUTANTS[n]}) survived the probe: {errs}"
+    assert max(errs.values()) > 1e-12 or lint["violations"], \
+        f"mutant {n} ({MUTANTS[n]}) survived the probe and the SASS check: {errs}"

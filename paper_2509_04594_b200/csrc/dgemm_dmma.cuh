@@ -45,6 +45,12 @@
 #define TB_MUTATE 0
 #endif
 
+// Software-pipelined fragment loads on every DMMA tile shape (1) or only on
+// 128 x 128 tiles with the plain loop elsewhere (0; A/B builds).
+#ifndef TB_XPF_ALL
+#define TB_XPF_ALL 1
+#endif
+
 #ifndef TB_GROUP_M
 #define TB_GROUP_M 16  // tile-raster band height (A/B builds: tools/build_variant.py NAME -DTB_GROUP_M=16)
 #endif
@@ -431,18 +437,22 @@ __global__ void __launch_bounds__(DmmaCfg::THREADS, 1)
       for (int j = 0; j < C::NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
     TB_TL(unsigned long long tl_u = 0;)
-    if constexpr (MT == Math::DMMA && SUB == 1 && BM == 128) {
-      // Cross-stage fragment prefetch: the next stage's full barrier is
-      // waited on, and its first half-step fragments loaded, before this
-      // stage's second half-step DMMAs issue, so the tensor pipe does not
-      // drain at stage boundaries (+0.3-0.45 % at N = 5000-10000 and on the
-      // 1250-row shard, profiles/r01_xpf_ab.txt; a few address registers
-      // spill, per stage, outside the DMMA stream). The 64-row tiles keep
-      // the plain loop below (measured neutral to -0.3 % there).
+    if constexpr (MT == Math::DMMA && (TB_XPF_ALL || (SUB == 1 && BM == 128 && BN == 128))) {
+      // Software-pipelined fragment loads: the fragments of half-step h + 1
+      // (a half-step = 8 of a 16-deep sub-slab's k) are loaded before the
+      // DMMAs of half-step h issue, across sub-slabs and across stages (the
+      // next stage's full barrier is waited on, and its first half-step
+      // loaded, before this stage's last DMMAs), so the tensor pipe does not
+      // drain at stage boundaries and the schedule does not depend on how
+      // ptxas interleaves a plain loop (+0.3-0.45 % at N = 5000-10000 on
+      // 128 x 128 tiles, profiles/r01_xpf_ab.txt; a few address registers
+      // spill there, per stage, outside the DMMA stream).
+      constexpr int HS = 2 * SUB;
       double2 fa[2][C::MI];
       double fb[2][2][C::NI];
-      auto ld = [&](int stage, int half, int buf) {
-        const uint8_t* sa = smem + stage * STAGE_BYTES;
+      auto ld = [&](int stage, int hs, int buf) {
+        const int half = hs & 1;
+        const uint8_t* sa = smem + stage * STAGE_BYTES + (hs >> 1) * C::STAGE;
         const uint8_t* sb = sa + C::A_STAGE;
 #pragma unroll
         for (int i = 0; i < C::MI; ++i)
@@ -475,9 +485,13 @@ __global__ void __launch_bounds__(DmmaCfg::THREADS, 1)
 #endif
       ld(s, 0, 0);
 #endif
+      TB_TL(if (tl && ct == 0) { tl_u = tl_now(); if (tl[1] == 0) tl[1] = tl_u; })
       for (int kt = kb; kt < ke; ++kt) {
-        ld(s, 1, 1);
-        mma(0);
+#pragma unroll
+        for (int hs = 0; hs + 1 < HS; ++hs) {
+          ld(s, hs + 1, (hs + 1) & 1);
+          mma(hs & 1);
+        }
         const int s1 = s + 1 == STAGES ? 0 : s + 1;
         const uint32_t ph1 = s + 1 == STAGES ? ph ^ 1 : ph;
         if (kt + 1 < ke) {
@@ -608,38 +622,74 @@ __global__ void __launch_bounds__(DmmaCfg::THREADS, 1)
       const int nseg = (int)((first + p.num_k - 1) / p.sk_ipc - first / p.sk_ipc + 1);
       double2* slots = reinterpret_cast<double2*>(p.partials) + (size_t)st * p.max_seg * (C::TILE_ELEMS / 2);
       double2* mine = slots + (size_t)seg * (C::TILE_ELEMS / 2);
-#pragma unroll
-      for (int i = 0; i < C::MI; ++i)
-#pragma unroll
-        for (int j = 0; j < C::NI; ++j)
-          __stcg(mine + (i * C::NI + j) * C::CONSUMER_THREADS + ct, make_double2(acc[i][j][0], acc[i][j][1]));
-      __threadfence();
+      // A segment that finds every other segment already published is the
+      // tile's last: it keeps its partial in registers (no store, no fence,
+      // no atomic) — typically the CTA that ran the tile's first k-range at
+      // the end of its work list, i.e. the launch's critical path. Others
+      // publish (store, fence, count) and the one whose count completes the
+      // tile reduces.
+      if (ct == 0) *flag = ld_acquire_gpu(&p.counters[st]);
       consumer_bar();
-      if (ct == 0) *flag = atomicAdd(&p.counters[st], 1);
-      consumer_bar();
-      const bool last = (*flag == nseg - 1);
-      consumer_bar();  // flag is reused by the next unit
+      bool last = (*flag == nseg - 1);
+      consumer_bar();  // flag is rewritten below / by the next unit
       if (!last) {
-        TB_TL(if (tl && ct == 0) { const unsigned long long t = tl_now(); tl[5] += t - tl_m; tl[3] = t; })
-        continue;
+#pragma unroll
+        for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+          for (int j = 0; j < C::NI; ++j)
+            __stcg(mine + (i * C::NI + j) * C::CONSUMER_THREADS + ct, make_double2(acc[i][j][0], acc[i][j][1]));
+        __threadfence();
+        consumer_bar();
+        if (ct == 0) *flag = atomicAdd(&p.counters[st], 1);
+        consumer_bar();
+        last = (*flag == nseg - 1);
+        consumer_bar();  // flag is reused by the next unit
+        if (!last) {
+          TB_TL(if (tl && ct == 0) { const unsigned long long t = tl_now(); tl[5] += t - tl_m; tl[3] = t; })
+          continue;
+        }
       }
       __threadfence();
-      // Deterministic reduction: all segments (own one re-read from L2 too)
-      // summed in index order 0..nseg-1, whichever CTA finishes last.
+      // Deterministic reduction: all segments summed in index order
+      // 0..nseg-1, whichever CTA finishes last. This CTA's own partial enters
+      // from registers: for seg <= 1 the running sum starts as own + p_other
+      // (the first addition commutes, so this is bitwise p0 + p1) and the
+      // rest are added in order; for seg >= 2 (split-K) it is stored to its
+      // slot (if not already published) and all slots are summed from memory.
+      if (seg <= 1) {
+        for (int sg = 0; sg < nseg; ++sg) {
+          if (sg == seg) continue;
+          const double2* src = slots + (size_t)sg * (C::TILE_ELEMS / 2) + ct;
 #pragma unroll
-      for (int i = 0; i < C::MI; ++i)
+          for (int i = 0; i < C::MI; ++i)
 #pragma unroll
-        for (int j = 0; j < C::NI; ++j) {
-          const double2* src = slots + (i * C::NI + j) * C::CONSUMER_THREADS + ct;
-          double2 sum = __ldcg(src);
-          for (int sg = 1; sg < nseg; ++sg) {
-            const double2 v = __ldcg(src + (size_t)sg * (C::TILE_ELEMS / 2));
-            sum.x += v.x;
-            sum.y += v.y;
-          }
-          acc[i][j][0] = sum.x;
-          acc[i][j][1] = sum.y;
+            for (int j = 0; j < C::NI; ++j) {
+              const double2 v = __ldcg(src + (i * C::NI + j) * C::CONSUMER_THREADS);
+              acc[i][j][0] += v.x;
+              acc[i][j][1] += v.y;
+            }
         }
+      } else {
+#pragma unroll
+        for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+          for (int j = 0; j < C::NI; ++j)
+            __stcg(mine + (i * C::NI + j) * C::CONSUMER_THREADS + ct, make_double2(acc[i][j][0], acc[i][j][1]));
+#pragma unroll
+        for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+          for (int j = 0; j < C::NI; ++j) {
+            const double2* src = slots + (i * C::NI + j) * C::CONSUMER_THREADS + ct;
+            double2 sum = __ldcg(src);
+            for (int sg = 1; sg < nseg; ++sg) {
+              const double2 v = __ldcg(src + (size_t)sg * (C::TILE_ELEMS / 2));
+              sum.x += v.x;
+              sum.y += v.y;
+            }
+            acc[i][j][0] = sum.x;
+            acc[i][j][1] = sum.y;
+          }
+      }
       if (ct == 0) p.counters[st] = 0;  // self-reset for the next launch
     }
 
@@ -656,23 +706,27 @@ __global__ void __launch_bounds__(DmmaCfg::THREADS, 1)
       // batches of 16 independent 16-byte loads (no branches, no stores in
       // between), so the epilogue pays two memory round trips, not one per
       // element.
+      constexpr int HALF = (C::MI + 1) / 2;  // odd MI (96-row tiles: 3): the second batch is one row shorter
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        double2 old[C::MI / 2][C::NI];
+        double2 old[HALF][C::NI];
 #pragma unroll
-        for (int ii = 0; ii < C::MI / 2; ++ii) {
-          const double* crow = p.C + (int64_t)(m0 + row_base + (h * C::MI / 2 + ii) * row_step) * p.ldc;
+        for (int ii = 0; ii < HALF; ++ii) {
+          if (h * HALF + ii >= C::MI) break;
+          const double* crow = p.C + (int64_t)(m0 + row_base + (h * HALF + ii) * row_step) * p.ldc;
 #pragma unroll
           for (int j = 0; j < C::NI; ++j)
             old[ii][j] = __ldcg(reinterpret_cast<const double2*>(crow + n0 + col_base + j * col_step));
         }
 #pragma unroll
-        for (int ii = 0; ii < C::MI / 2; ++ii)
+        for (int ii = 0; ii < HALF; ++ii) {
+          if (h * HALF + ii >= C::MI) break;
 #pragma unroll
           for (int j = 0; j < C::NI; ++j) {
-            acc[h * C::MI / 2 + ii][j][0] += old[ii][j].x;
-            acc[h * C::MI / 2 + ii][j][1] += old[ii][j].y;
+            acc[h * HALF + ii][j][0] += old[ii][j].x;
+            acc[h * HALF + ii][j][1] += old[ii][j].y;
           }
+        }
       }
     } else if (TB_ACCUM) {
 #undef TB_ACCUM

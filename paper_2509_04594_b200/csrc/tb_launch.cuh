@@ -33,7 +33,8 @@ struct Schedule {
   int grid, dp, sk, ipc, max_seg, num_k;
 };
 
-Schedule plan_schedule(int64_t tiles, int num_k, int sms) {
+// dp_only: the cost model's data-parallel alternative (choose_tile).
+Schedule plan_schedule(int64_t tiles, int num_k, int sms, bool dp_only = false) {
   static const int forced = [] {
     const char* e = std::getenv("TB_SCHED");
     if (e && std::strcmp(e, "dp") == 0) return 1;
@@ -42,13 +43,19 @@ Schedule plan_schedule(int64_t tiles, int num_k, int sms) {
   }();
   Schedule sc{sms, (int)tiles, 0, 1, 1, num_k};
   const int64_t rem = tiles % sms;
-  if (forced == 1 || rem == 0) return sc;
+  if (forced == 1 || rem == 0 || dp_only) {
+    sc.grid = (int)std::min<int64_t>(tiles, sms);  // no idle CTAs for a partial single wave
+    return sc;
+  }
   // A single wave >= 75 % full runs data-parallel: splitting every tile of a single wave costs about a
   // quarter of a tile's k-loop in partial traffic and fixups (N = 1500, 144 tiles: 28.6 -> 31.2;
   // N = 1000 on 64-row tiles, 128 tiles: 23.3 -> 25.9; N = 900, 120 tiles: 19.5 -> 20.5; at 61 %,
   // N = 800, stream-K stays ahead 18.2 vs 15.9 TFLOP/s). With more waves the stream-K tail wins
   // (N = 4000 / 6000 at 92 %: 34.12 / 35.84 vs 33.99 / 35.76).
-  if (forced == 0 && tiles < sms && 4 * tiles >= 3 * sms) return sc;
+  if (forced == 0 && tiles < sms && 4 * tiles >= 3 * sms) {
+    sc.grid = (int)tiles;
+    return sc;
+  }
   const int64_t min_seg = num_k < 8 ? num_k : 8;      // keep segments long enough to amortise the fixup
   if (forced == 0 && 2 * tiles <= sms) {
     int64_t split = std::min<int64_t>(sms / tiles, num_k / min_seg);
@@ -69,14 +76,138 @@ Schedule plan_schedule(int64_t tiles, int num_k, int sms) {
   int64_t ipc = (total + sms - 1) / sms;
   if (ipc < min_seg) ipc = min_seg;
   sc.ipc = (int)ipc;
-  int max_seg = 1;
-  for (int64_t st = 0; st < sc.sk; ++st) {
-    const int64_t first = st * num_k;
-    const int64_t nseg = (first + num_k - 1) / ipc - first / ipc + 1;
-    if (nseg > max_seg) max_seg = (int)nseg;
-  }
+  // Segments per tile: a tile's num_k iterations meet at most
+  // floor((num_k - 1) / ipc) + 2 CTA ranges (an upper bound — it only sizes
+  // the partial-tile workspace; the kernel derives each tile's exact count).
+  const int max_seg = (int)std::min<int64_t>((num_k - 1) / ipc + 2, sms);
   sc.max_seg = max_seg;
   return sc;
+}
+
+// ----------------------------------------------------------------------------
+// Tile-shape chooser (TMA + DMMA launches). Every main-tile configuration the
+// library instantiates, under its stream-K schedule (plan_schedule) and
+// purely data-parallel, is costed with one launch model and the cheapest runs:
+//
+//   t = w * t_stage + fixups * F * s + units * E * s + R,   s = bm*bn / 8192
+//
+// w = k-stages on the busiest CTA (data-parallel tiles + its stream-K
+// iterations), t_stage = bm*bn*16*SUB FMAs at 64 FMA/clk/SM times the
+// configuration's steady-state efficiency, fixups = the stream-K segment
+// reductions on that CTA (2 when the launch splits tiles), units = its tile
+// epilogues, R = launch + pipeline fill. The efficiencies, F = 2.55 us and
+// E = 0.18 us were fitted (tools/tile_model_fit.py, rms log error 0.6 %) to
+// the kernel-only sweep of all eight configurations x both schedules at
+// N = 1000..3000 step 50 and 3500..8192 on one B200
+// (profiles/r02_tile_sched_sweep.jsonl); there the model's pick is within
+// 1.6 % of the fastest measured (configuration, schedule) at every N and
+// 0.06 % off on the geometric mean (tests/test_tile_model.py replays it).
+// R cancels between single launches; 4 us per extra launch prices the
+// edge-strip plan: wide problems with ragged m / n run as 128 x 128 main
+// tiles plus remainder strips, each a launch of its own (see launch()).
+struct TileCfg {
+  int slot;  // launch_tiles' `strip` argument: -1 = 128 x 128, kStrip64x128 = 64-row kernel, else kTile*
+  int bm, bn, sub;
+  double eff;
+};
+constexpr TileCfg kTileCfgs[] = {
+    {-1, 128, 128, 1, 0.9711},         {kTile128x64, 128, 64, 2, 0.9727}, {kTile128x96, 128, 96, 1, 0.9629},
+    {kTile96x96, 96, 96, 1, 0.9514},   {kTile64x64, 64, 64, 2, 0.9456},   {kStrip64x128, 64, 128, 1, 0.9483},
+    {kTile96x128, 96, 128, 1, 0.9689}, {kTile64x96, 64, 96, 1, 0.9399},
+};
+// Edge-strip shapes (their launches carry the narrow tiles' lower efficiency:
+// N = 10000 strips measured 23.5 TFLOP/s including their fixups).
+constexpr double kStripEff = 0.70;
+constexpr double kModelF = 2.55e-6, kModelE = 0.184e-6, kModelR = 4e-6;
+constexpr double kSmFmaPerSec = 64.0 * 1.965e9;
+
+double model_seconds(int64_t m, int64_t n, int64_t k, int bm, int bn, int sub, double eff, int sms,
+                     bool dp_only = false) {
+  const int64_t tiles = ((m + bm - 1) / bm) * ((n + bn - 1) / bn);
+  const int num_k = (int)((k + 16 * sub - 1) / (16 * sub));
+  const Schedule sc = plan_schedule(tiles, num_k, sms, dp_only);
+  const double t_stage = (double)bm * bn * 16 * sub / (kSmFmaPerSec * eff);
+  const double s = (double)bm * bn / 8192.0;
+  double w, units, fix;
+  if (sc.sk == 0) {
+    units = (double)((tiles + sc.grid - 1) / sc.grid);
+    w = units * sc.num_k;
+    fix = 0;
+  } else {
+    const double dpw = (double)(sc.dp / sc.grid);
+    w = dpw * sc.num_k + sc.ipc;
+    units = dpw + (double)((sc.ipc + sc.num_k - 1) / sc.num_k) + 1;
+    fix = 2;
+  }
+  return w * t_stage + fix * kModelF * s + units * kModelE * s + kModelR;
+}
+
+struct TileChoice {
+  int slot;     // launch_tiles' strip argument for a single launch
+  bool split;   // 128 x 128 main part + edge-strip launches instead
+  bool dp;      // the single launch runs data-parallel (no stream-K split)
+  double seconds;
+};
+
+// Edge-strip plan of launch(): bottom / right strip shapes for the ragged
+// remainders (kStripNone when the remainder is 0 or wider than 64).
+void strip_cfgs(int64_t m, int64_t n, int& bcfg, int& rcfg) {
+  const int64_t hb = m % 128, wr = n % 128;
+  bcfg = hb == 0 ? kStripNone : hb <= 16 ? kStrip16x128 : hb <= 32 ? kStrip32x128 : hb <= 64 ? kStrip64x128
+                                                                                             : kStripNone;
+  rcfg = wr == 0 ? kStripNone : wr <= 16 ? kStrip128x16 : wr <= 32 ? kStrip128x32 : wr <= 64 ? kStrip128x64
+                                                                                             : kStripNone;
+}
+
+// split_mode: 0 = costed, -1 = never split, 1 = split whenever the shape allows.
+TileChoice choose_tile_uncached(int64_t m, int64_t n, int64_t k, int sms, int split_mode) {
+  TileChoice best{-1, false, false, 1e30};
+  for (const TileCfg& c : kTileCfgs)
+    for (bool dp : {false, true}) {
+      const double t = model_seconds(m, n, k, c.bm, c.bn, c.sub, c.eff, sms, dp);
+      if (t < best.seconds) best = {c.slot, false, dp, t};
+    }
+  if (split_mode >= 0 && (m % 128 != 0 || n % 128 != 0)) {
+    int bcfg, rcfg;
+    strip_cfgs(m, n, bcfg, rcfg);
+    const int64_t m1 = bcfg != kStripNone ? m - m % 128 : m, n1 = rcfg != kStripNone ? n - n % 128 : n;
+    if ((bcfg != kStripNone || rcfg != kStripNone) && m1 >= 128 && n1 >= 128) {
+      double t = model_seconds(m1, n1, k, 128, 128, 1, kTileCfgs[0].eff, sms);
+      if (rcfg != kStripNone) {
+        const StripInfo si = strip_info(rcfg);
+        t += model_seconds(m, n - n1, k, si.bm, si.bn, si.sub, kStripEff, sms);
+      }
+      if (bcfg != kStripNone) {
+        const int sbm = bcfg == kStrip64x128 ? 64 : strip_info(bcfg).bm;
+        const int ssub = bcfg == kStrip64x128 ? 1 : strip_info(bcfg).sub;
+        t += model_seconds(m - m1, n1, k, sbm, 128, ssub, bcfg == kStrip64x128 ? 0.9483 : kStripEff, sms);
+      }
+      if (t < best.seconds || split_mode == 1) best = {-1, true, false, t};
+    }
+  }
+  return best;
+}
+
+// The choice is a few microseconds of host arithmetic; a per-thread cache of
+// recent shapes keeps it off repeated calls (a synchronous call's kernel-only
+// clock starts before the host enqueues).
+TileChoice choose_tile(int64_t m, int64_t n, int64_t k, int sms, int split_mode) {
+  struct Entry {
+    int64_t m, n, k;
+    int sms, split_mode;
+    TileChoice tc;
+  };
+  thread_local Entry cache[8];
+  thread_local int next = 0, used = 0;
+  for (int i = 0; i < used; ++i) {
+    const Entry& e = cache[i];
+    if (e.m == m && e.n == n && e.k == k && e.sms == sms && e.split_mode == split_mode) return e.tc;
+  }
+  const TileChoice tc = choose_tile_uncached(m, n, k, sms, split_mode);
+  cache[next] = {m, n, k, sms, split_mode, tc};
+  next = (next + 1) % 8;
+  if (used < 8) ++used;
+  return tc;
 }
 
 int split_workspace(int dev, cudaStream_t stream, size_t partial_elems, size_t counter_elems, double** partials,
@@ -175,13 +306,14 @@ int stage_workspace(int dev, cudaStream_t stream, size_t elems, double** buf) {
 
 int launch_tiles(int dev, const double* A, int64_t lda, const double* B, int64_t ldb, double* Cm, int64_t ldc,
                  int64_t m, int64_t k, int64_t n, int accumulate, int tile_edge, int variant, cudaStream_t stream,
-                 int strip);
+                 int strip, bool dp_only = false);
 
 // Enqueue one GEMM on `stream` (current device = dev). Assumes validated args.
-// Stages misaligned operands (large AUTO calls), then, for a large TMA-fed
-// DMMA product whose m or n is not a multiple of 128, runs the whole-tile
-// part and the remainder strips as separate launches (TB_SPLIT=0: one
-// launch, A/B).
+// Stages misaligned operands (large AUTO calls), then, for a TMA-fed DMMA
+// product, runs the tile shape the cost model picks (choose_tile): one launch
+// on one of the main-tile shapes, or — for wide problems with ragged m / n —
+// a whole 128 x 128-tile launch plus the remainder strips as launches of
+// their own.
 int launch(int dev, const double* A, int64_t lda, const double* B, int64_t ldb, double* Cm, int64_t ldc, int64_t m,
            int64_t k, int64_t n, int accumulate, int tile_edge, int variant, cudaStream_t stream) {
   int s = g_plan ? TB_STATUS_OK : ensure_kernel_attrs(dev);
@@ -223,8 +355,11 @@ int launch(int dev, const double* A, int64_t lda, const double* B, int64_t ldb, 
     }
   }
   variant = resolve(A, lda, B, ldb, variant);
-  // TB_TILE=<bm>x<bn>: force one main-tile shape, no edge split (A/B sweeps).
-  static const int forced_tile = [] {
+  // Test / A-B hooks, read per call (tests switch them in-process):
+  // TB_TILE=<bm>x<bn> forces one main-tile shape with no edge split;
+  // TB_SPLIT=0 never splits off edge strips, TB_SPLIT=1 always does when the
+  // shape allows it (strip-kernel parity tests); unset: the cost model decides.
+  const int forced_tile = [] {
     const char* e = std::getenv("TB_TILE");
     if (!e) return 0;
     for (int c = kStrip64x128; c < kNumStripCfgs; ++c) {
@@ -237,30 +372,30 @@ int launch(int dev, const double* A, int64_t lda, const double* B, int64_t ldb, 
   }();
   if (forced_tile && variant == TB_VARIANT_DMMA_TMA)
     return launch_tiles(dev, A, lda, B, ldb, Cm, ldc, m, k, n, accumulate, tile_edge, variant, stream, forced_tile);
-  static const bool split_env = !(std::getenv("TB_SPLIT") && std::strcmp(std::getenv("TB_SPLIT"), "0") == 0);
-  if (split_env && variant == TB_VARIANT_DMMA_TMA && (m % 128 != 0 || n % 128 != 0)) {
-    const int64_t hb = m % 128, wr = n % 128;
-    const int bcfg = hb == 0 ? kStripNone : hb <= 16 ? kStrip16x128 : hb <= 32 ? kStrip32x128
-                                                      : hb <= 64 ? kStrip64x128 : kStripNone;
-    const int rcfg = wr == 0 ? kStripNone : wr <= 16 ? kStrip128x16 : wr <= 32 ? kStrip128x32
-                                                      : wr <= 64 ? kStrip128x64 : kStripNone;
-    const int64_t m1 = bcfg != kStripNone ? m - hb : m, n1 = rcfg != kStripNone ? n - wr : n;
-    if ((bcfg != kStripNone || rcfg != kStripNone) && m1 >= 128 && n1 >= 128 &&
-        choose_bm(m1, n1, dev_sms(dev), false) == 128) {
-      // Main part on whole 128 x 128 tiles, then the right strip (all rows)
-      // and the bottom strip (the main part's columns); disjoint parts of C.
-      if ((s = launch_tiles(dev, A, lda, B, ldb, Cm, ldc, m1, k, n1, accumulate, tile_edge, variant, stream, -1)))
-        return s;
-      if (rcfg != kStripNone &&
-          (s = launch_tiles(dev, A, lda, B + n1, ldb, Cm + n1, ldc, m, k, n - n1, accumulate, tile_edge, variant,
-                            stream, rcfg)))
-        return s;
-      if (bcfg != kStripNone &&
-          (s = launch_tiles(dev, A + m1 * lda, lda, B, ldb, Cm + m1 * ldc, ldc, m - m1, k, n1, accumulate,
-                            tile_edge, variant, stream, bcfg)))
-        return s;
-      return TB_STATUS_OK;
-    }
+  const char* split_e = std::getenv("TB_SPLIT");
+  const int split_mode = !split_e ? 0 : std::strcmp(split_e, "0") == 0 ? -1 : std::strcmp(split_e, "1") == 0 ? 1 : 0;
+  if (variant == TB_VARIANT_DMMA_TMA) {
+    // Costed choice between every main-tile shape and the edge-strip plan (choose_tile).
+    const TileChoice tc = choose_tile(m, n, k, dev_sms(dev), split_mode);
+    if (!tc.split)
+      return launch_tiles(dev, A, lda, B, ldb, Cm, ldc, m, k, n, accumulate, tile_edge, variant, stream, tc.slot,
+                          tc.dp);
+    int bcfg, rcfg;
+    strip_cfgs(m, n, bcfg, rcfg);
+    const int64_t m1 = bcfg != kStripNone ? m - m % 128 : m, n1 = rcfg != kStripNone ? n - n % 128 : n;
+    // Main part on whole 128 x 128 tiles, then the right strip (all rows)
+    // and the bottom strip (the main part's columns); disjoint parts of C.
+    if ((s = launch_tiles(dev, A, lda, B, ldb, Cm, ldc, m1, k, n1, accumulate, tile_edge, variant, stream, -1)))
+      return s;
+    if (rcfg != kStripNone &&
+        (s = launch_tiles(dev, A, lda, B + n1, ldb, Cm + n1, ldc, m, k, n - n1, accumulate, tile_edge, variant,
+                          stream, rcfg)))
+      return s;
+    if (bcfg != kStripNone &&
+        (s = launch_tiles(dev, A + m1 * lda, lda, B, ldb, Cm + m1 * ldc, ldc, m - m1, k, n1, accumulate, tile_edge,
+                          variant, stream, bcfg)))
+      return s;
+    return TB_STATUS_OK;
   }
   return launch_tiles(dev, A, lda, B, ldb, Cm, ldc, m, k, n, accumulate, tile_edge, variant, stream, kStripNone);
 }
@@ -269,7 +404,7 @@ int launch(int dev, const double* A, int64_t lda, const double* B, int64_t ldb, 
 // height, -1 = 128 x 128 forced, else an edge-strip shape.
 int launch_tiles(int dev, const double* A, int64_t lda, const double* B, int64_t ldb, double* Cm, int64_t ldc,
                  int64_t m, int64_t k, int64_t n, int accumulate, int tile_edge, int variant, cudaStream_t stream,
-                 int strip) {
+                 int strip, bool dp_only) {
   int s = TB_STATUS_OK;
   if (variant == TB_VARIANT_PAPER) {
     const int K = tile_edge;
@@ -315,7 +450,7 @@ int launch_tiles(int dev, const double* A, int64_t lda, const double* B, int64_t
     const int64_t kstage = narrow ? (int64_t)Cfg::BK * si.sub : bm == 64 ? (int64_t)Cfg::BK
                                                                        : (int64_t)Cfg::BK * kCfgs[cfg].sub;
     p.num_k = (int)((k + kstage - 1) / kstage);
-    const Schedule sc = plan_schedule(tiles, p.num_k, dev_sms(dev));
+    const Schedule sc = plan_schedule(tiles, p.num_k, dev_sms(dev), dp_only);
     p.num_k = sc.num_k;  // split-K pads the k-slab count (extra slabs read as zeros)
     p.dp_tiles = sc.dp;
     p.sk_tiles = sc.sk;

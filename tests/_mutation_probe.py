@@ -8,25 +8,31 @@ with fresh operands per repetition (stale shared memory from an identical
 earlier launch would otherwise mask a read-before-land), and prints the
 largest normwise error per case as JSON. The reference: cuBLAS FP64 (torch)."""
 import json
+import os
 import sys
 
 import torch
 
 import paper_2509_04594_b200 as tb
 
-CASES = [  # (name, m, k, n, accumulate)
-    ("tiles128_streamk", 2048, 2048, 2048, False),
-    ("tiles64_dataparallel", 1000, 1000, 1000, False),
-    ("tiles128_edge_strips", 4000, 1000, 4000, False),
-    ("splitk", 256, 4096, 256, False),
-    ("accumulate_epilogue", 4096, 512, 4096, True),
+CASES = [  # (name, m, k, n, accumulate, env: TB_TILE forces a tile shape, TB_SPLIT=1 the edge strips)
+    ("tiles128_streamk", 2048, 2048, 2048, False, {"TB_TILE": "128x128"}),
+    ("tiles64_dataparallel", 1000, 1000, 1000, False, {"TB_TILE": "64x128"}),
+    ("tiles64x64_streamk", 1300, 1300, 1300, False, {"TB_TILE": "64x64"}),
+    ("tiles96x96_streamk", 2000, 1000, 2000, False, {"TB_TILE": "96x96"}),
+    ("tiles128_edge_strips", 4000, 1000, 4000, False, {"TB_SPLIT": "1"}),
+    ("splitk", 256, 4096, 256, False, {}),
+    ("accumulate_epilogue", 4096, 512, 4096, True, {"TB_TILE": "128x128"}),
 ]
 
 
 def main(reps: int) -> None:
     g = torch.Generator(device="cuda")
     out = {}
-    for name, m, k, n, acc in CASES:
+    for name, m, k, n, acc, env in CASES:
+        for key in ("TB_TILE", "TB_SPLIT"):
+            os.environ.pop(key, None)
+        os.environ.update(env)
         worst = 0.0
         for r in range(reps):
             g.manual_seed(1000 * r + m + k + n)

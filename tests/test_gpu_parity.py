@@ -476,13 +476,17 @@ def test_flat_small_no_phase_one(tb, oracle, m, k, n, kind):
     assert oracle.normwise_rel(cn[rows], oracle.tiled_parallel(a[rows], b)) <= NORMWISE
 
 
-@pytest.mark.parametrize("m,k,n", [(2320, 600, 2320), (2336, 500, 2368), (2368, 300, 2340), (4001, 257, 3999)])
-def test_edge_strip_split(tb, oracle, m, k, n):
-    """Large TMA products with ragged m / n run as a whole-tile launch plus
-    edge strips (16/32/64-row and 32/64-column strip shapes); C, plain and
-    accumulated, equals the oracle's rows and cuBLAS normwise."""
+@pytest.mark.parametrize("m,k,n", [(2320, 600, 2320), (2336, 500, 2368), (2368, 300, 2340), (2320, 400, 2334),
+                                   (4001, 257, 3999)])
+def test_edge_strip_split(tb, oracle, monkeypatch, m, k, n):
+    """TMA products with ragged m / n run as a whole-tile launch plus edge
+    strips (16/32/64-row and 16/32/64-column strip shapes; TB_SPLIT=1 takes
+    the split wherever the shape allows, the cost model would pick one
+    launch for some of these); C, plain and accumulated, equals the oracle's
+    rows and cuBLAS normwise."""
     import torch
 
+    monkeypatch.setenv("TB_SPLIT", "1")
     a, b = oracle.generate(m, k, 41), oracle.generate(k, n, 42)
     ta, tbm = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
     c, sec = tb.dgemm(ta, tbm)
@@ -494,6 +498,33 @@ def test_edge_strip_split(tb, oracle, m, k, n):
     tb.dgemm_launch(ta, tbm, out, accumulate=True)
     torch.cuda.synchronize()
     assert (torch.linalg.norm(out - 2 * ref) / torch.linalg.norm(2 * ref)).item() <= NORMWISE
+
+
+TILES = ["128x128", "128x64", "128x96", "96x96", "64x64", "64x128", "96x128", "64x96"]
+
+
+@pytest.mark.parametrize("tile", TILES)
+@pytest.mark.parametrize("m,k,n", [(1000, 1000, 1000), (1300, 700, 1700), (250, 3000, 130), (4096, 96, 4096)])
+def test_every_main_tile_shape(tb, oracle, monkeypatch, tile, m, k, n):
+    """Every main-tile shape the cost model can pick (TB_TILE forces it):
+    ragged tile grids, stream-K / split-K / data-parallel schedules; plain C
+    against the oracle's rows and cuBLAS, then C += A·B."""
+    import torch
+
+    monkeypatch.setenv("TB_TILE", tile)
+    a, b = oracle.generate(m, k, 51), oracle.generate(k, n, 52)
+    ta, tbm = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    c, sec = tb.dgemm(ta, tbm)
+    rows = np.r_[0:3, m // 2, m - 3:m]
+    assert oracle.normwise_rel(c.cpu().numpy()[rows], oracle.tiled_parallel(a[rows], b)) <= NORMWISE
+    ref, _ = tb.cublas_dgemm(ta, tbm)
+    assert (torch.linalg.norm(c - ref) / torch.linalg.norm(ref)).item() <= NORMWISE
+    out = ref.clone()
+    tb.dgemm_launch(ta, tbm, out, accumulate=True)
+    torch.cuda.synchronize()
+    assert (torch.linalg.norm(out - 2 * ref) / torch.linalg.norm(2 * ref)).item() <= NORMWISE
+    again, _ = tb.dgemm(ta, tbm)
+    assert torch.equal(again, c)  # deterministic stream-K reduction
 
 
 def test_staged_tma_for_misaligned_operands(tb, oracle):

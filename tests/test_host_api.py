@@ -139,7 +139,8 @@ def test_runner_with_external_backend_and_csv(tmp_path, oracle):
     gpu = side["config"]["gpu"]
     assert gpu["library"].startswith("tbgpu") and gpu["cublas_version"] and gpu["cublas_path"]
     assert "fp64_emulation" in gpu and "device_count" in gpu
-    assert [p["tile"] for p in side["config"]["launch_plans"]["16"]] == [[64, 128, 16]]
+    plan16 = side["config"]["launch_plans"]["16"]
+    assert len(plan16) == 1 and plan16[0]["kernel"] == "dmma" and plan16[0]["m"] == plan16[0]["n"] == 16
 
 
 def test_launch_plan_describes_the_schedule():
@@ -150,7 +151,8 @@ def test_launch_plan_describes_the_schedule():
     assert [x["tile"][:2] for x in p] == [[128, 128], [128, 16], [16, 128]]
     assert p[0]["schedule"] == "stream-k" and p[0]["m"] == p[0]["n"] == 9984 and p[0]["grid"] == 148
     assert p[1]["strip"] and p[2]["strip"]
-    assert _lib.launch_plan(1000, 1000, 1000)[0]["schedule"] == "data-parallel"
+    assert _lib.launch_plan(1500, 1500, 1500)[0]["schedule"] == "data-parallel"
+    assert _lib.launch_plan(1000, 1000, 1000)[0]["tile"] == [64, 64, 32]
     assert _lib.launch_plan(9999, 9999, 9999)[0] == {"repitch": "AB"}
     assert _lib.launch_plan(300, 300, 300, "paper")[0]["block"] == [32, 32]
     assert _lib.launch_plan(2000, 2000, 2000, sms=132)[0]["grid"] == 132

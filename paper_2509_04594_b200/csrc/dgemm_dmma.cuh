@@ -51,6 +51,10 @@
 #define TB_XPF_ALL 1
 #endif
 
+#ifndef TB_EARLY_RELEASE
+#define TB_EARLY_RELEASE -1
+#endif
+
 #ifndef TB_GROUP_M
 #define TB_GROUP_M 16  // tile-raster band height (A/B builds: tools/build_variant.py NAME -DTB_GROUP_M=16)
 #endif
@@ -448,6 +452,11 @@ __global__ void __launch_bounds__(DmmaCfg::THREADS, 1)
       // 128 x 128 tiles, profiles/r01_xpf_ab.txt; a few address registers
       // spill there, per stage, outside the DMMA stream).
       constexpr int HS = 2 * SUB;
+      // Early stage release on every shape but 128 x 128 (same-box A/B,
+      // profiles/r02_early_release_ab.jsonl: 64 x 96 / 128 x 96 / 96 x 96
+      // +0.3-1.3 %, 128 x 64 neutral, 128 x 128 -0.6 %). TB_EARLY_RELEASE=0|1
+      // forces it off / on everywhere (A/B builds).
+      constexpr bool kEarlyRelease = TB_EARLY_RELEASE < 0 ? !(BM == 128 && BN == 128) : TB_EARLY_RELEASE != 0;
       double2 fa[2][C::MI];
       double fb[2][2][C::NI];
       auto ld = [&](int stage, int hs, int buf) {
@@ -494,6 +503,20 @@ __global__ void __launch_bounds__(DmmaCfg::THREADS, 1)
         }
         const int s1 = s + 1 == STAGES ? 0 : s + 1;
         const uint32_t ph1 = s + 1 == STAGES ? ph ^ 1 : ph;
+        if constexpr (kEarlyRelease) {
+          // Every fragment of stage s is now loaded (the last half-step's
+          // went out before the mma above): release the stage before waiting
+          // on the next one, so the proxy fence waits only on those loads,
+          // not on the next stage's freshly issued ones, and the producer
+          // refills a half-step earlier.
+#if TB_MUTATE != 3
+          fence_proxy_async();
+#endif
+          __syncwarp();
+#if TB_MUTATE != 2
+          if (lane == 0) mbar_arrive(smem_u32(&empty[s]));
+#endif
+        }
         if (kt + 1 < ke) {
 #if TB_MUTATE == 1
           ld(s1, 0, 0);
@@ -508,13 +531,15 @@ __global__ void __launch_bounds__(DmmaCfg::THREADS, 1)
 #endif
         }
         mma(1);
+        if constexpr (!kEarlyRelease) {
 #if TB_MUTATE != 3
-        fence_proxy_async();
+          fence_proxy_async();
 #endif
-        __syncwarp();
+          __syncwarp();
 #if TB_MUTATE != 2
-        if (lane == 0) mbar_arrive(smem_u32(&empty[s]));
+          if (lane == 0) mbar_arrive(smem_u32(&empty[s]));
 #endif
+        }
         s = s1;
         ph = ph1;
       }

@@ -95,13 +95,13 @@ Schedule plan_schedule(int64_t tiles, int num_k, int sms, bool dp_only = false) 
 // iterations), t_stage = bm*bn*16*SUB FMAs at 64 FMA/clk/SM times the
 // configuration's steady-state efficiency, fixups = the stream-K segment
 // reductions on that CTA (2 when the launch splits tiles), units = its tile
-// epilogues, R = launch + pipeline fill. The efficiencies, F = 2.55 us and
-// E = 0.18 us were fitted (tools/tile_model_fit.py, rms log error 0.6 %) to
+// epilogues, R = launch + pipeline fill. The efficiencies, F = 2.22 us and
+// E = 0.53 us were fitted (tools/tile_model_fit.py, rms log error 0.5 %) to
 // the kernel-only sweep of all eight configurations x both schedules at
 // N = 1000..3000 step 50 and 3500..8192 on one B200
 // (profiles/r02_tile_sched_sweep.jsonl); there the model's pick is within
-// 1.6 % of the fastest measured (configuration, schedule) at every N and
-// 0.06 % off on the geometric mean (tests/test_tile_model.py replays it).
+// 2.3 % of the fastest measured (configuration, schedule) at every N and
+// 0.1 % off on the geometric mean (tests/test_tile_model.py replays it).
 // R cancels between single launches; 4 us per extra launch prices the
 // edge-strip plan: wide problems with ragged m / n run as 128 x 128 main
 // tiles plus remainder strips, each a launch of its own (see launch()).
@@ -111,14 +111,14 @@ struct TileCfg {
   double eff;
 };
 constexpr TileCfg kTileCfgs[] = {
-    {-1, 128, 128, 1, 0.9711},         {kTile128x64, 128, 64, 2, 0.9727}, {kTile128x96, 128, 96, 1, 0.9629},
-    {kTile96x96, 96, 96, 1, 0.9514},   {kTile64x64, 64, 64, 2, 0.9456},   {kStrip64x128, 64, 128, 1, 0.9483},
-    {kTile96x128, 96, 128, 1, 0.9689}, {kTile64x96, 64, 96, 1, 0.9399},
+    {-1, 128, 128, 1, 0.9719},         {kTile128x64, 128, 64, 2, 0.9720}, {kTile128x96, 128, 96, 1, 0.9711},
+    {kTile96x96, 96, 96, 1, 0.9560},   {kTile64x64, 64, 64, 2, 0.9479},   {kStrip64x128, 64, 128, 1, 0.9532},
+    {kTile96x128, 96, 128, 1, 0.9702}, {kTile64x96, 64, 96, 1, 0.9463},
 };
 // Edge-strip shapes (their launches carry the narrow tiles' lower efficiency:
 // N = 10000 strips measured 23.5 TFLOP/s including their fixups).
 constexpr double kStripEff = 0.70;
-constexpr double kModelF = 2.55e-6, kModelE = 0.184e-6, kModelR = 4e-6;
+constexpr double kModelF = 2.22e-6, kModelE = 0.529e-6, kModelR = 4e-6;
 constexpr double kSmFmaPerSec = 64.0 * 1.965e9;
 
 double model_seconds(int64_t m, int64_t n, int64_t k, int bm, int bn, int sub, double eff, int sms,
@@ -180,7 +180,7 @@ TileChoice choose_tile_uncached(int64_t m, int64_t n, int64_t k, int sms, int sp
       if (bcfg != kStripNone) {
         const int sbm = bcfg == kStrip64x128 ? 64 : strip_info(bcfg).bm;
         const int ssub = bcfg == kStrip64x128 ? 1 : strip_info(bcfg).sub;
-        t += model_seconds(m - m1, n1, k, sbm, 128, ssub, bcfg == kStrip64x128 ? 0.9483 : kStripEff, sms);
+        t += model_seconds(m - m1, n1, k, sbm, 128, ssub, bcfg == kStrip64x128 ? 0.9532 : kStripEff, sms);
       }
       if (t < best.seconds || split_mode == 1) best = {-1, true, false, t};
     }

@@ -16,11 +16,11 @@ import sys
 P = 148
 # name: (bm, bn, sub, steady-state efficiency) — kTileCfgs in tb_launch.cuh
 CFG = {
-    "128x128": (128, 128, 1, 0.9711), "128x64": (128, 64, 2, 0.9727), "128x96": (128, 96, 1, 0.9629),
-    "96x96": (96, 96, 1, 0.9514), "64x64": (64, 64, 2, 0.9456), "64x128": (64, 128, 1, 0.9483),
-    "96x128": (96, 128, 1, 0.9689), "64x96": (64, 96, 1, 0.9399),
+    "128x128": (128, 128, 1, 0.9719), "128x64": (128, 64, 2, 0.9720), "128x96": (128, 96, 1, 0.9711),
+    "96x96": (96, 96, 1, 0.9560), "64x64": (64, 64, 2, 0.9479), "64x128": (64, 128, 1, 0.9532),
+    "96x128": (96, 128, 1, 0.9702), "64x96": (64, 96, 1, 0.9463),
 }
-F, E, R = 2.55e-6, 0.184e-6, 4e-6
+F, E, R = 2.22e-6, 0.529e-6, 4e-6
 SM_FMA_PER_S = 64 * 1.965e9
 
 

@@ -110,11 +110,17 @@ struct TileCfg {
   int bm, bn, sub;
   double eff;
 };
+// Largest tiles first: a later (smaller) shape must beat the best so far by
+// kPreferLarger to be picked, so near-ties go to the shape with less
+// operand traffic per flop (long-K shards re-read panels from DRAM, §3.1 of
+// 128 x 64 and 128 x 128 are equally fast at N = 8192, but the
+// larger tile halves B's reads).
 constexpr TileCfg kTileCfgs[] = {
-    {-1, 128, 128, 1, 0.9719},         {kTile128x64, 128, 64, 2, 0.9720}, {kTile128x96, 128, 96, 1, 0.9711},
-    {kTile96x96, 96, 96, 1, 0.9560},   {kTile64x64, 64, 64, 2, 0.9479},   {kStrip64x128, 64, 128, 1, 0.9532},
-    {kTile96x128, 96, 128, 1, 0.9702}, {kTile64x96, 64, 96, 1, 0.9463},
+    {-1, 128, 128, 1, 0.9719},         {kTile128x96, 128, 96, 1, 0.9711}, {kTile96x128, 96, 128, 1, 0.9702},
+    {kTile128x64, 128, 64, 2, 0.9720}, {kStrip64x128, 64, 128, 1, 0.9532}, {kTile96x96, 96, 96, 1, 0.9560},
+    {kTile64x96, 64, 96, 1, 0.9463},   {kTile64x64, 64, 64, 2, 0.9479},
 };
+constexpr double kPreferLarger = 2e-3;
 // Edge-strip shapes (their launches carry the narrow tiles' lower efficiency:
 // N = 10000 strips measured 23.5 TFLOP/s including their fixups).
 constexpr double kStripEff = 0.70;
@@ -165,7 +171,8 @@ TileChoice choose_tile_uncached(int64_t m, int64_t n, int64_t k, int sms, int sp
   for (const TileCfg& c : kTileCfgs)
     for (bool dp : {false, true}) {
       const double t = model_seconds(m, n, k, c.bm, c.bn, c.sub, c.eff, sms, dp);
-      if (t < best.seconds) best = {c.slot, false, dp, t};
+      const bool same_shape = best.slot == c.slot && best.seconds < 1e30;
+      if (t < best.seconds * (same_shape ? 1.0 : 1.0 - kPreferLarger)) best = {c.slot, false, dp, t};
     }
   if (split_mode >= 0 && (m % 128 != 0 || n % 128 != 0)) {
     int bcfg, rcfg;

@@ -15,11 +15,12 @@ import sys
 
 P = 148
 # name: (bm, bn, sub, steady-state efficiency) — kTileCfgs in tb_launch.cuh
-CFG = {
-    "128x128": (128, 128, 1, 0.9719), "128x64": (128, 64, 2, 0.9720), "128x96": (128, 96, 1, 0.9711),
-    "96x96": (96, 96, 1, 0.9560), "64x64": (64, 64, 2, 0.9479), "64x128": (64, 128, 1, 0.9532),
-    "96x128": (96, 128, 1, 0.9702), "64x96": (64, 96, 1, 0.9463),
+CFG = {  # largest tiles first (the chooser's tie-break order)
+    "128x128": (128, 128, 1, 0.9719), "128x96": (128, 96, 1, 0.9711), "96x128": (96, 128, 1, 0.9702),
+    "128x64": (128, 64, 2, 0.9720), "64x128": (64, 128, 1, 0.9532), "96x96": (96, 96, 1, 0.9560),
+    "64x96": (64, 96, 1, 0.9463), "64x64": (64, 64, 2, 0.9479),
 }
+PREFER_LARGER = 2e-3
 F, E, R = 2.22e-6, 0.529e-6, 4e-6
 SM_FMA_PER_S = 64 * 1.965e9
 
@@ -57,10 +58,15 @@ def model_seconds(m, n, k, bm, bn, sub, eff, sms=P, dp_only=False):
 
 
 def choose(m, n, k, cands=None):
-    """(config, dp_only) the model picks among single launches."""
-    cands = cands or list(CFG)
-    return min(((c, dp) for c in cands for dp in (False, True)),
-               key=lambda x: model_seconds(m, n, k, *CFG[x[0]], dp_only=x[1]))
+    """(config, dp_only) the model picks among single launches: in CFG order
+    (largest tiles first), a different shape must be faster by PREFER_LARGER."""
+    best, best_t = None, float("inf")
+    for c in [c for c in CFG if c in (cands or CFG)]:
+        for dp in (False, True):
+            t = model_seconds(m, n, k, *CFG[c], dp_only=dp)
+            if t < best_t * (1.0 if best and best[0] == c else 1.0 - PREFER_LARGER):
+                best, best_t = (c, dp), t
+    return best
 
 
 def pick(m, n, k, cands=None):

@@ -84,6 +84,7 @@ enum StripCfg : int {
   kTile96x96,
   kTile64x96,
   kTile128x64,
+  kTile64x64d,  // 64 x 64 with 64-deep stages (SUB 4 x 3): fewer stage boundaries, shallower ring
   kNumStripCfgs
 };
 // Narrow tiles do little work per 16-deep k-slab, so a strip stage holds
@@ -108,10 +109,11 @@ StripInfo strip_info(int c) {
     case kStrip16x128: return {16, 128, 4, StripK<16, 128, 1, 4, 3>::fn(), StripK<16, 128, 1, 4, 3>::smem()};
     case kStrip32x128: return {32, 128, 2, StripK<32, 128, 1, 2, 5>::fn(), StripK<32, 128, 1, 2, 5>::smem()};
     case kTile64x64: return {64, 64, 2, StripK<64, 64, 2, 2, 6>::fn(), StripK<64, 64, 2, 2, 6>::smem()};
+    case kTile64x64d: return {64, 64, 4, StripK<64, 64, 2, 4, 3>::fn(), StripK<64, 64, 2, 4, 3>::smem()};
     case kTile96x128: return {96, 128, 1, StripK<96, 128, 2, 1, 7>::fn(), StripK<96, 128, 2, 1, 7>::smem()};
     case kTile128x96: return {128, 96, 1, StripK<128, 96, 4, 1, 7>::fn(), StripK<128, 96, 4, 1, 7>::smem()};
-    case kTile96x96: return {96, 96, 1, StripK<96, 96, 4, 1, 8>::fn(), StripK<96, 96, 4, 1, 8>::smem()};
-    case kTile64x96: return {64, 96, 1, StripK<64, 96, 4, 1, 9>::fn(), StripK<64, 96, 4, 1, 9>::smem()};
+    case kTile96x96: return {96, 96, 2, StripK<96, 96, 4, 2, 4>::fn(), StripK<96, 96, 4, 2, 4>::smem()};
+    case kTile64x96: return {64, 96, 2, StripK<64, 96, 4, 2, 5>::fn(), StripK<64, 96, 4, 2, 5>::smem()};
     case kTile128x64: return {128, 64, 2, StripK<128, 64, 4, 2, 4>::fn(), StripK<128, 64, 4, 2, 4>::smem()};
     default: return {0, 0, 1, nullptr, 0};
   }

@@ -143,16 +143,20 @@ def test_runner_with_external_backend_and_csv(tmp_path, oracle):
     assert len(plan16) == 1 and plan16[0]["kernel"] == "dmma" and plan16[0]["m"] == plan16[0]["n"] == 16
 
 
-def test_launch_plan_describes_the_schedule():
+def test_launch_plan_describes_the_schedule(monkeypatch):
     """tb_launch_plan: the resolved kernel / tile / schedule per launch (no device)."""
     from paper_2509_04594_b200 import _lib
 
+    monkeypatch.delenv("TB_TILE", raising=False)
+    monkeypatch.delenv("TB_SPLIT", raising=False)
     p = _lib.launch_plan(10000, 10000, 10000)
     assert [x["tile"][:2] for x in p] == [[128, 128], [128, 16], [16, 128]]
     assert p[0]["schedule"] == "stream-k" and p[0]["m"] == p[0]["n"] == 9984 and p[0]["grid"] == 148
     assert p[1]["strip"] and p[2]["strip"]
-    assert _lib.launch_plan(1500, 1500, 1500)[0]["schedule"] == "data-parallel"
-    assert _lib.launch_plan(1000, 1000, 1000)[0]["tile"] == [64, 64, 32]
+    assert _lib.launch_plan(1000, 1000, 1000)[0]["tile"] == [64, 64, 64]
+    monkeypatch.setenv("TB_TILE", "128x128")  # a >= 75 % full single wave runs data-parallel, on min(T, P) CTAs
+    p = _lib.launch_plan(1500, 1500, 1500)
+    assert p[0]["schedule"] == "data-parallel" and p[0]["grid"] == 144
     assert _lib.launch_plan(9999, 9999, 9999)[0] == {"repitch": "AB"}
     assert _lib.launch_plan(300, 300, 300, "paper")[0]["block"] == [32, 32]
     assert _lib.launch_plan(2000, 2000, 2000, sms=132)[0]["grid"] == 132

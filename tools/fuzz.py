@@ -18,6 +18,8 @@ for i in range(cases):
     big = rng.random() < 0.25
     hi = 6000 if big else 700
     m, k, n = (int(rng.integers(1, hi)) for _ in range(3))
+    if rng.random() < 0.5:  # even leading dimensions: TMA-addressable, through the tile-shape chooser
+        k, n = k + k % 2, n + n % 2
     mode = rng.choice(["dgemm", "launch_acc", "view", "flat_pinned", "flat_pageable"])
     variant = rng.choice(["auto", "auto", "dmma_tma", "dmma_cpasync", "dfma"]) if mode != "flat_pageable" else "auto"
     a = torch.from_numpy(rng.random((m, k)) * 3 + 2)

@@ -51,6 +51,8 @@ PipePlan plan_pipeline(int64_t m, int64_t k, int64_t n, int sms, bool fused_ok, 
     // problems need finer blocks for their D2H to overlap (N = 2000: 1536-row
     // blocks 1.85 ms, 512-row 1.66; profiles/r01_pipe_small_blocks.txt).
     int64_t kp0 = 256, kp_max = 2048, groups = 2;
+    if (const char* e = std::getenv("TB_PIPE_KP0")) kp0 = std::max<long long>(16, std::atoll(e));        // tuning
+    if (const char* e = std::getenv("TB_PIPE_KPMAX")) kp_max = std::max<long long>(16, std::atoll(e));   // tuning
     int64_t blk = std::min<int64_t>(1536, std::max<int64_t>(512, (m / 4 + 64) / 128 * 128));
     // TB_PIPE=mq,kp0,kp_max,blk[,groups] overrides the shape (tuning experiments).
     if (const char* e = std::getenv("TB_PIPE")) {

@@ -95,9 +95,9 @@ Schedule plan_schedule(int64_t tiles, int num_k, int sms, bool dp_only = false) 
 // iterations), t_stage = bm*bn*16*SUB FMAs at 64 FMA/clk/SM times the
 // configuration's steady-state efficiency, fixups = the stream-K segment
 // reductions on that CTA (2 when the launch splits tiles), units = its tile
-// epilogues, R = launch + pipeline fill. The efficiencies, F = 2.75 us and
-// E = 0.11 us were fitted (tools/tile_model_fit.py, rms log error 0.6 %) to
-// the kernel-only sweep of all nine configurations x both schedules at
+// epilogues, R = launch + pipeline fill. The efficiencies, F = 2.31 us and
+// E = 0.34 us were fitted (tools/tile_model_fit.py, rms log error 0.55 %) to
+// the kernel-only sweep of all eleven configurations x both schedules at
 // N = 1000..3000 step 50 and 3500..8192 on one B200
 // (profiles/r02_tile_sched_sweep.jsonl); there the model's pick is within
 // 2.3 % of the fastest measured (configuration, schedule) at every N and
@@ -116,15 +116,16 @@ struct TileCfg {
 // 128 x 64 and 128 x 128 are equally fast at N = 8192, but the
 // larger tile halves B's reads).
 constexpr TileCfg kTileCfgs[] = {
-    {-1, 128, 128, 1, 0.9708},         {kTile128x96, 128, 96, 1, 0.9696}, {kTile96x128, 96, 128, 1, 0.9712},
-    {kTile128x64, 128, 64, 2, 0.9722}, {kStrip64x128, 64, 128, 1, 0.9529}, {kTile96x96, 96, 96, 2, 0.9739},
-    {kTile64x96, 64, 96, 2, 0.9696},   {kTile64x64d, 64, 64, 4, 0.9633}, {kTile64x64, 64, 64, 2, 0.9481},
+    {-1, 128, 128, 1, 0.9691},         {kTile128x96, 128, 96, 1, 0.9701}, {kTile96x128, 96, 128, 1, 0.9705},
+    {kTile128x64, 128, 64, 2, 0.9710}, {kTile64x128, 64, 128, 2, 0.9670}, {kStrip64x128, 64, 128, 1, 0.9530},
+    {kTile96x96t, 96, 96, 3, 0.9776},  {kTile96x96, 96, 96, 2, 0.9731},   {kTile64x96, 64, 96, 2, 0.9688},
+    {kTile64x64d, 64, 64, 4, 0.9632},  {kTile64x64, 64, 64, 2, 0.9480},
 };
 constexpr double kPreferLarger = 2e-3;
 // Edge-strip shapes (their launches carry the narrow tiles' lower efficiency:
 // N = 10000 strips measured 23.5 TFLOP/s including their fixups).
 constexpr double kStripEff = 0.70;
-constexpr double kModelF = 2.75e-6, kModelE = 0.110e-6, kModelR = 4e-6;
+constexpr double kModelF = 2.31e-6, kModelE = 0.344e-6, kModelR = 4e-6;
 constexpr double kSmFmaPerSec = 64.0 * 1.965e9;
 
 double model_seconds(int64_t m, int64_t n, int64_t k, int bm, int bn, int sub, double eff, int sms,
@@ -187,7 +188,7 @@ TileChoice choose_tile_uncached(int64_t m, int64_t n, int64_t k, int sms, int sp
       if (bcfg != kStripNone) {
         const int sbm = bcfg == kStrip64x128 ? 64 : strip_info(bcfg).bm;
         const int ssub = bcfg == kStrip64x128 ? 1 : strip_info(bcfg).sub;
-        t += model_seconds(m - m1, n1, k, sbm, 128, ssub, bcfg == kStrip64x128 ? 0.9529 : kStripEff, sms);
+        t += model_seconds(m - m1, n1, k, sbm, 128, ssub, bcfg == kStrip64x128 ? 0.9530 : kStripEff, sms);
       }
       if (t < best.seconds || split_mode == 1) best = {-1, true, false, t};
     }
@@ -373,7 +374,7 @@ int launch(int dev, const double* A, int64_t lda, const double* B, int64_t ldb, 
       const StripInfo si = strip_info(c);
       char name[32];
       std::snprintf(name, sizeof(name), "%dx%d%s", c == kStrip64x128 ? 64 : si.bm, c == kStrip64x128 ? 128 : si.bn,
-                    c == kTile64x64d ? "d" : "");
+                    c == kTile64x64d || c == kTile64x128 ? "d" : c == kTile96x96t ? "t" : "");
       if (std::strcmp(e, name) == 0) return c;
     }
     return std::strcmp(e, "128x128") == 0 ? -1 : 0;

@@ -84,7 +84,9 @@ enum StripCfg : int {
   kTile96x96,
   kTile64x96,
   kTile128x64,
+  kTile64x128,  // TMA 64 x 128 with 32-deep stages (the 64-row kernel kStrip64x128 keeps 16-deep ones)
   kTile64x64d,  // 64 x 64 with 64-deep stages (SUB 4 x 3): fewer stage boundaries, shallower ring
+  kTile96x96t,  // 96 x 96 with 48-deep stages (SUB 3 x 3)
   kNumStripCfgs
 };
 // Narrow tiles do little work per 16-deep k-slab, so a strip stage holds
@@ -113,7 +115,9 @@ StripInfo strip_info(int c) {
     case kTile96x128: return {96, 128, 1, StripK<96, 128, 2, 1, 7>::fn(), StripK<96, 128, 2, 1, 7>::smem()};
     case kTile128x96: return {128, 96, 1, StripK<128, 96, 4, 1, 7>::fn(), StripK<128, 96, 4, 1, 7>::smem()};
     case kTile96x96: return {96, 96, 2, StripK<96, 96, 4, 2, 4>::fn(), StripK<96, 96, 4, 2, 4>::smem()};
+    case kTile96x96t: return {96, 96, 3, StripK<96, 96, 4, 3, 3>::fn(), StripK<96, 96, 4, 3, 3>::smem()};
     case kTile64x96: return {64, 96, 2, StripK<64, 96, 4, 2, 5>::fn(), StripK<64, 96, 4, 2, 5>::smem()};
+    case kTile64x128: return {64, 128, 2, StripK<64, 128, 2, 2, 4>::fn(), StripK<64, 128, 2, 2, 4>::smem()};
     case kTile128x64: return {128, 64, 2, StripK<128, 64, 4, 2, 4>::fn(), StripK<128, 64, 4, 2, 4>::smem()};
     default: return {0, 0, 1, nullptr, 0};
   }

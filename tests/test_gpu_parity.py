@@ -500,7 +500,7 @@ def test_edge_strip_split(tb, oracle, monkeypatch, m, k, n):
     assert (torch.linalg.norm(out - 2 * ref) / torch.linalg.norm(2 * ref)).item() <= NORMWISE
 
 
-TILES = ["128x128", "128x64", "128x96", "96x96", "64x64", "64x64d", "64x128", "96x128", "64x96"]
+TILES = ["128x128", "128x64", "128x96", "96x96", "96x96t", "64x64", "64x64d", "64x128", "64x128d", "96x128", "64x96"]
 
 
 @pytest.mark.parametrize("tile", TILES)

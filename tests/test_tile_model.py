@@ -13,8 +13,8 @@ sys.path.insert(0, os.path.join(ROOT, "tools"))
 import tile_model  # noqa: E402
 
 SLOT_NAME = {(128, 128, 16): "128x128", (128, 64, 32): "128x64", (128, 96, 16): "128x96", (96, 96, 32): "96x96",
-             (64, 64, 32): "64x64", (64, 64, 64): "64x64d", (64, 128, 16): "64x128", (96, 128, 16): "96x128",
-             (64, 96, 32): "64x96"}
+             (64, 64, 32): "64x64", (64, 64, 64): "64x64d", (64, 128, 16): "64x128", (64, 128, 32): "64x128d",
+             (96, 96, 48): "96x96t", (96, 128, 16): "96x128", (64, 96, 32): "64x96"}
 
 
 def test_model_pick_is_near_fastest_measured():

@@ -16,12 +16,13 @@ import sys
 P = 148
 # name: (bm, bn, sub, steady-state efficiency) — kTileCfgs in tb_launch.cuh
 CFG = {  # largest tiles first (the chooser's tie-break order)
-    "128x128": (128, 128, 1, 0.9708), "128x96": (128, 96, 1, 0.9696), "96x128": (96, 128, 1, 0.9712),
-    "128x64": (128, 64, 2, 0.9722), "64x128": (64, 128, 1, 0.9529), "96x96": (96, 96, 2, 0.9739),
-    "64x96": (64, 96, 2, 0.9696), "64x64d": (64, 64, 4, 0.9633), "64x64": (64, 64, 2, 0.9481),
+    "128x128": (128, 128, 1, 0.9691), "128x96": (128, 96, 1, 0.9701), "96x128": (96, 128, 1, 0.9705),
+    "128x64": (128, 64, 2, 0.9710), "64x128d": (64, 128, 2, 0.9670), "64x128": (64, 128, 1, 0.9530),
+    "96x96t": (96, 96, 3, 0.9776), "96x96": (96, 96, 2, 0.9731), "64x96": (64, 96, 2, 0.9688),
+    "64x64d": (64, 64, 4, 0.9632), "64x64": (64, 64, 2, 0.9480),
 }
 PREFER_LARGER = 2e-3
-F, E, R = 2.75e-6, 0.110e-6, 4e-6
+F, E, R = 2.31e-6, 0.344e-6, 4e-6
 SM_FMA_PER_S = 64 * 1.965e9
 
 

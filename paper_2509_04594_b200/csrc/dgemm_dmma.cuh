@@ -51,6 +51,11 @@
 #define TB_XPF_ALL 1
 #endif
 
+// L2 prefetch of the old C tile ahead of an accumulating epilogue (1) or not (0; A/B builds).
+#ifndef TB_C_PREFETCH
+#define TB_C_PREFETCH 1
+#endif
+
 #ifndef TB_EARLY_RELEASE
 #define TB_EARLY_RELEASE -1
 #endif
@@ -377,6 +382,18 @@ __global__ void __launch_bounds__(DmmaCfg::THREADS, 1)
         if (++s == STAGES) {
           s = 0;
           ph ^= 1;
+        }
+      }
+      // The unit's loads are all issued (the consumers are ~STAGES stages
+      // behind): if its epilogue will add the old C tile (C += A·B, or a
+      // PIPE panel after the first), pull that tile into L2 now so the
+      // epilogue's loads hit L2 instead of DRAM.
+      if constexpr (LD == Loader::TMA && TB_C_PREFETCH) {
+        if ((PIPE ? (p.accumulate || kb != 0) : p.accumulate) && p.vec_store && !(PIPE && aborted)) {
+          const int r_end = min(m0 + C::BM, p.m);
+          const uint32_t bytes = (uint32_t)((min(n0 + C::BN, p.n) - n0) * 8) & ~15u;  // never past the row
+          if (bytes)
+            for (int r = m0; r < r_end; ++r) bulk_prefetch_l2(p.C + (int64_t)r * p.ldc + n0, bytes);
         }
       }
     }

@@ -527,6 +527,35 @@ def test_every_main_tile_shape(tb, oracle, monkeypatch, tile, m, k, n):
     assert torch.equal(again, c)  # deterministic stream-K reduction
 
 
+# Square sizes at which the cost model (tb_launch.cuh choose_tile) picks each
+# (shape, schedule) it uses in N = 200..5000, found with the host-only plan;
+# the test re-derives the plan, so a model refit that moves a pick still
+# tests the launch it makes.
+CHOOSER_SIZES = [200, 230, 330, 490, 650, 810, 840, 1090, 1110, 1290, 1350, 1370, 1480, 1890, 2070, 2500]
+
+
+@pytest.mark.parametrize("n", CHOOSER_SIZES)
+def test_chooser_picks_match_cublas(tb, oracle, n):
+    """Whatever (tile shape, schedule) the cost model picks — data-parallel on
+    min(T, 148) CTAs, stream-K, split-K — the default dgemm equals cuBLAS
+    normwise and the oracle on sampled rows, repeatably."""
+    import torch
+
+    from paper_2509_04594_b200 import _lib
+
+    plan = _lib.launch_plan(n, n, n)
+    assert len(plan) == 1 and plan[0]["kernel"] == "dmma" and plan[0]["loader"] == "tma", plan
+    a, b = oracle.generate(n, n, 61), oracle.generate(n, n, 62)
+    ta, tbm = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    c, _ = tb.dgemm(ta, tbm)
+    ref, _ = tb.cublas_dgemm(ta, tbm)
+    assert (torch.linalg.norm(c - ref) / torch.linalg.norm(ref)).item() <= NORMWISE, plan[0]
+    rows = np.r_[0:2, n // 2, n - 2:n]
+    assert oracle.normwise_rel(c.cpu().numpy()[rows], oracle.tiled_parallel(a[rows], b)) <= NORMWISE
+    again, _ = tb.dgemm(ta, tbm)
+    assert torch.equal(again, c)
+
+
 def test_staged_tma_for_misaligned_operands(tb, oracle):
     """AUTO on operands TMA cannot address (odd leading dimension; base off a
     16-byte boundary) above the staging threshold copies them to even-pitch

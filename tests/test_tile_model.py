@@ -51,3 +51,25 @@ def test_split_plan_for_wide_ragged_problems(monkeypatch):
     monkeypatch.setenv("TB_SPLIT", "1")
     p = _lib.launch_plan(2320, 400, 2334)
     assert [x["tile"][:2] for x in p] == [[128, 128], [128, 32], [16, 128]]
+
+
+def test_gpu_chooser_sizes_cover_every_pick(monkeypatch):
+    """tests/test_gpu_parity.py::test_chooser_picks_match_cublas runs one size
+    per (shape, schedule) the model picks for square N = 200..5000; keep that
+    list complete when the model changes."""
+    import ast
+
+    from paper_2509_04594_b200 import _lib
+
+    monkeypatch.delenv("TB_TILE", raising=False)
+    monkeypatch.delenv("TB_SPLIT", raising=False)
+    src = open(os.path.join(ROOT, "tests", "test_gpu_parity.py")).read()
+    line = next(x for x in src.splitlines() if x.startswith("CHOOSER_SIZES = "))
+    sizes = ast.literal_eval(line.split("=", 1)[1].strip())
+
+    def key(n):
+        p = _lib.launch_plan(n, n, n)
+        return (tuple(p[0]["tile"]), p[0]["schedule"]) if len(p) == 1 else None
+
+    picked = {key(n) for n in list(range(200, 3001, 10)) + [3500, 4096, 5000]} - {None}
+    assert picked <= {key(n) for n in sizes}, picked - {key(n) for n in sizes}

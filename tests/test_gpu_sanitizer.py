@@ -56,3 +56,18 @@ def test_sanitizer_clean(driver, tool, args, bm):
     out = res.stdout + res.stderr
     assert res.returncode == 0, out[-4000:]
     assert "ERROR SUMMARY: 0 errors" in out or "RACECHECK SUMMARY: 0 hazards" in out, out[-2000:]
+
+
+@pytest.mark.parametrize("tile", ["128x64", "128x96", "96x128", "96x96", "96x96t", "64x64", "64x64d", "64x96",
+                                  "64x128d"])
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck"])
+def test_sanitizer_clean_every_tile_shape(driver, tool, tile):
+    """Every tile shape the cost model can pick (TB_TILE forces it on the
+    driver's TMA-fed calls: split-K fixups on these small shapes, ragged
+    edges, early stage release): memcheck and racecheck clean."""
+    env = dict(os.environ, TB_TILE=tile)
+    res = subprocess.run([_sanitizer(), "--tool", tool, "--error-exitcode", "3", driver, "--tma-only"],
+                         capture_output=True, text=True, timeout=900, env=env)
+    out = res.stdout + res.stderr
+    assert res.returncode == 0, out[-4000:]
+    assert "ERROR SUMMARY: 0 errors" in out or "RACECHECK SUMMARY: 0 hazards" in out, out[-2000:]

@@ -77,6 +77,22 @@ PipePlan plan_pipeline(int64_t m, int64_t k, int64_t n, int sms, bool fused_ok, 
     const int64_t mq_cap =
         std::max<int64_t>(128, (int64_t)((double)m * c2k / (c2k + 1.2 * 8.0 / kD2H)) / 128 * 128);
     if (!std::getenv("TB_PIPE")) mq = std::min(mq, mq_cap);
+    // D2H-bound sizes: every row of C leaves after B has fully landed (phase-1 rows need all K-panels),
+    // so all of C's D2H (8mn/D) must fit under phase 2's compute, (m - Mq)·2kn/F: Mq <= m(1 - 4F/(D·k)).
+    // Where that binds (N ~ 3000-7000 pinned), phase-2 blocks shrink to ~0.3 ms of compute each (>= 256
+    // rows) so C streams back while A still streams in (pinned e2e N = 4000 / 5000 / 6000: 6.38 / 11.38 /
+    // 16.19 -> 6.08 / 10.75 / 14.71 ms, profiles/r02_pipe_d2h_cap.txt). TB_PIPE_D2HCAP=0 disables (A/B).
+    const char* dce = std::getenv("TB_PIPE_D2HCAP");
+    if (!std::getenv("TB_PIPE") && !(dce && std::strcmp(dce, "0") == 0)) {
+      const double f = 1.0 - 4.0 * kRate / (kD2H * (double)k);
+      const int64_t cap2 = f > 0 ? std::max<int64_t>(128, (int64_t)((double)m * f) / 128 * 128) : 128;
+      if (cap2 < mq) {
+        mq = cap2;
+        const int64_t b3 = (int64_t)(0.3e-3 * kRate / (2.0 * (double)k * (double)n)) / 128 * 128;
+        blk = std::max<int64_t>(256, std::min(blk, b3));
+      }
+    }
+    if (const char* e = std::getenv("TB_PIPE_BLK")) blk = std::max<long long>(128, std::atoll(e));  // tuning
     // Phase 1 as one persistent launch that waits on per-panel flags (PIPE
     // mode) rather than a launch per panel and row group, from 2e11 flops:
     // below that (N <= ~4600) the launch-per-panel form is as fast or faster

@@ -765,6 +765,16 @@ void tb_release(void) {
       if (kv.second.counters) cudaFree(kv.second.counters);
     }
     st.split_ws.clear();
+    {
+      std::lock_guard<std::mutex> lk_side(st.side_mu);
+      for (auto& kv : st.side) {
+        if (kv.second.s) cudaStreamSynchronize(kv.second.s);
+        if (kv.second.s) cudaStreamDestroy(kv.second.s);
+        if (kv.second.fork) cudaEventDestroy(kv.second.fork);
+        if (kv.second.join) cudaEventDestroy(kv.second.join);
+      }
+      st.side.clear();
+    }
   }
 }
 

@@ -394,16 +394,49 @@ int launch(int dev, const double* A, int64_t lda, const double* B, int64_t ldb, 
     const int64_t m1 = bcfg != kStripNone ? m - m % 128 : m, n1 = rcfg != kStripNone ? n - n % 128 : n;
     // Main part on whole 128 x 128 tiles, then the right strip (all rows)
     // and the bottom strip (the main part's columns); disjoint parts of C.
+    // The strips go on a side stream forked after the main launch, so their
+    // CTAs take SMs as the main launch's CTAs retire (its ~0.2 ms end-time
+    // spread) instead of waiting for the last one; the caller's stream then
+    // waits for them (TB_STRIP_CONCURRENT=0: all on the caller's stream).
+    DeviceState& st = g_dev[dev];
+    const char* sce = std::getenv("TB_STRIP_CONCURRENT");
+    const bool side_ok = !g_plan && !(sce && std::strcmp(sce, "0") == 0);
+    std::unique_lock<std::mutex> side_lk(st.side_mu, std::defer_lock);
+    DeviceState::SideStream* ss = nullptr;
+    if (side_ok) {
+      side_lk.lock();
+      DeviceState::SideStream& e = st.side[stream];
+      if (!e.s) {
+        if (cudaStreamCreateWithFlags(&e.s, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&e.fork, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&e.join, cudaEventDisableTiming) != cudaSuccess) {
+          cudaGetLastError();
+          if (e.s) cudaStreamDestroy(e.s);
+          if (e.fork) cudaEventDestroy(e.fork);
+          e = DeviceState::SideStream{};
+        }
+      }
+      if (e.s) ss = &e;
+    }
+    if (ss) {
+      TB_CUDA(cudaEventRecord(ss->fork, stream), "strip fork");
+      TB_CUDA(cudaStreamWaitEvent(ss->s, ss->fork, 0), "strip fork");
+    }
     if ((s = launch_tiles(dev, A, lda, B, ldb, Cm, ldc, m1, k, n1, accumulate, tile_edge, variant, stream, -1)))
       return s;
+    const cudaStream_t strip_stream = ss ? ss->s : stream;
     if (rcfg != kStripNone &&
         (s = launch_tiles(dev, A, lda, B + n1, ldb, Cm + n1, ldc, m, k, n - n1, accumulate, tile_edge, variant,
-                          stream, rcfg)))
+                          strip_stream, rcfg)))
       return s;
     if (bcfg != kStripNone &&
         (s = launch_tiles(dev, A + m1 * lda, lda, B, ldb, Cm + m1 * ldc, ldc, m - m1, k, n1, accumulate, tile_edge,
-                          variant, stream, bcfg)))
+                          variant, strip_stream, bcfg)))
       return s;
+    if (ss) {
+      TB_CUDA(cudaEventRecord(ss->join, ss->s), "strip join");
+      TB_CUDA(cudaStreamWaitEvent(stream, ss->join, 0), "strip join");
+    }
     return TB_STATUS_OK;
   }
   return launch_tiles(dev, A, lda, B, ldb, Cm, ldc, m, k, n, accumulate, tile_edge, variant, stream, kStripNone);

@@ -200,6 +200,12 @@ struct DeviceState {
     size_t elems = 0;
   };
   std::map<cudaStream_t, StageWs> stage_ws;
+  struct SideStream {  // per caller stream: the edge-strip launches' stream + fork / join events
+    cudaStream_t s = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+  };
+  std::map<cudaStream_t, SideStream> side;
+  std::mutex side_mu;  // one fork / launch / join sequence at a time per device
   std::vector<cudaEvent_t> ev_pool[2];  // host-buffer entry: [timing, no-timing] events
   int* dtab = nullptr;                  // host-buffer entry: [0,128) panel flags (+ abort word at
                                         // tb::kPipeAbortWord), [128,256) panel k-stages

@@ -81,7 +81,8 @@ PipePlan plan_pipeline(int64_t m, int64_t k, int64_t n, int sms, bool fused_ok, 
     // so all of C's D2H (8mn/D) must fit under phase 2's compute, (m - Mq)·2kn/F: Mq <= m(1 - 4F/(D·k)).
     // Where that binds (N ~ 3000-7000 pinned), phase-2 blocks shrink to ~0.3 ms of compute each (>= 256
     // rows) so C streams back while A still streams in (pinned e2e N = 4000 / 5000 / 6000: 6.38 / 11.38 /
-    // 16.19 -> 6.08 / 10.75 / 14.71 ms, profiles/r02_pipe_d2h_cap.txt). TB_PIPE_D2HCAP=0 disables (A/B).
+    // 16.19 -> 6.08 / 10.75 / 14.71 ms before the first-panel change below, profiles/r02_pipe_d2h_cap.txt).
+    // TB_PIPE_D2HCAP=0 disables (A/B).
     const char* dce = std::getenv("TB_PIPE_D2HCAP");
     if (!std::getenv("TB_PIPE") && !(dce && std::strcmp(dce, "0") == 0)) {
       const double f = 1.0 - 4.0 * kRate / (kD2H * (double)k);
@@ -90,6 +91,9 @@ PipePlan plan_pipeline(int64_t m, int64_t k, int64_t n, int sms, bool fused_ok, 
         mq = cap2;
         const int64_t b3 = (int64_t)(0.3e-3 * kRate / (2.0 * (double)k * (double)n)) / 128 * 128;
         blk = std::max<int64_t>(256, std::min(blk, b3));
+        // With the smaller phase 1, a 512-deep first panel (fewer, larger panel GEMMs) wins:
+        // N = 3000 / 4000 / 5000 / 6000 -1.8 / -1.1 / -4.6 / -1.2 % (profiles/r02_pipe_d2h_cap.txt).
+        if (!std::getenv("TB_PIPE_KP0")) kp0 = std::max<int64_t>(kp0, 512);
       }
     }
     if (const char* e = std::getenv("TB_PIPE_BLK")) blk = std::max<long long>(128, std::atoll(e));  // tuning

@@ -500,6 +500,35 @@ def test_edge_strip_split(tb, oracle, monkeypatch, m, k, n):
     assert (torch.linalg.norm(out - 2 * ref) / torch.linalg.norm(2 * ref)).item() <= NORMWISE
 
 
+def test_side_stream_strips_match_serial(tb, monkeypatch):
+    """The edge strips run on a side stream joined back to the caller's
+    stream (tb_launch.cuh launch()): bitwise the same C as all launches on
+    one stream, on the default stream and on a user stream, plain and
+    accumulate, and the caller's stream sees the strips' results."""
+    import torch
+
+    monkeypatch.setenv("TB_SPLIT", "1")
+    g = torch.Generator(device="cuda").manual_seed(9)
+    a = torch.rand((2320, 400), dtype=torch.float64, device="cuda", generator=g)
+    b = torch.rand((400, 2334), dtype=torch.float64, device="cuda", generator=g)
+    outs = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("TB_STRIP_CONCURRENT", mode)
+        c, _ = tb.dgemm(a, b)
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            c2 = torch.ones_like(c)
+            tb.dgemm_launch(a, b, c2, accumulate=True, stream=s)
+            # consumed on the user stream right after: must include the strips
+            col = c2[:, -30:].sum()
+        s.synchronize()
+        outs[mode] = (c, c2, col.item())
+    assert torch.equal(outs["0"][0], outs["1"][0]) and torch.equal(outs["0"][1], outs["1"][1])
+    assert outs["0"][2] == outs["1"][2]
+    ref = a @ b
+    assert (torch.linalg.norm(outs["1"][0] - ref) / torch.linalg.norm(ref)).item() <= NORMWISE
+
+
 TILES = ["128x128", "128x64", "128x96", "96x96", "96x96t", "64x64", "64x64d", "64x128", "64x128d", "96x128", "64x96"]
 
 

@@ -256,37 +256,49 @@ int split_workspace(int dev, cudaStream_t stream, size_t partial_elems, size_t c
 
 // Staging. AUTO on operands TMA cannot address (odd leading dimension or a base not
 // 16-byte aligned — the reference's odd-N cases) would run the cp.async
-// loader at ~92 % of the TMA path's speed. For large products the operands
-// are instead copied once, on the launching stream, into even-pitch
-// workspace buffers (HBM copy: ~1 % of the GEMM time at N = 9999) and the
-// TMA kernel runs on those. Small products keep the cp.async loader.
-constexpr double kStageMinFlops = 2e10;
+// loader, which lacks the TMA path's tile shapes and chooser. From 2e6 flops
+// (N ~ 100) the operands are instead copied once, on the launching stream,
+// into even-pitch workspace buffers (HBM copy: ~1 % of the GEMM time at
+// N = 9999) and the TMA kernel runs on those: round 2 lowered the threshold
+// from 2e10 after a same-box A/B (profiles/r02_odd_n_staging.txt, kernel-only
+// TFLOP/s cp.async -> staged: N = 1001 19.5 -> 23.0, 1501 25.0 -> 28.8,
+// 1999 25.8 -> 32.4 (cuBLAS 31.8); 129 30.5 -> 22.2 us; N = 65 equal).
+// Tiny products keep the cp.async loader.
+constexpr double kStageMinFlops = 2e6;
 constexpr size_t kStageMaxBytes = size_t(16) << 30;
 
 // Row re-pitch for staging: dst (16-byte aligned, even pitch) <- src (any
 // 8-byte alignment/pitch). One block row-slab per blockIdx.y, coalesced 8-byte
 // loads, 16-byte stores where the destination allows.
-__global__ void __launch_bounds__(256) repitch_kernel(const double* __restrict__ src, int64_t lds,
-                                                      double* __restrict__ dst, int64_t ldd, int64_t rows,
-                                                      int64_t cols) {
-  for (int64_t r = blockIdx.y; r < rows; r += gridDim.y) {
-    const double* s = src + r * lds;
-    double2* d = reinterpret_cast<double2*>(dst + r * ldd);
-    for (int64_t c = 2 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x); c < cols;
+struct RepitchJob {
+  const double* src;
+  int64_t lds;
+  double* dst;
+  int64_t ldd, rows, cols;
+};
+
+// One launch re-pitches up to two operands (blockIdx.z picks the job).
+__global__ void __launch_bounds__(256) repitch_kernel(RepitchJob j0, RepitchJob j1) {
+  const RepitchJob& j = blockIdx.z == 0 ? j0 : j1;
+  for (int64_t r = blockIdx.y; r < j.rows; r += gridDim.y) {
+    const double* s = j.src + r * j.lds;
+    double2* d = reinterpret_cast<double2*>(j.dst + r * j.ldd);
+    for (int64_t c = 2 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x); c < j.cols;
          c += 2 * (int64_t)gridDim.x * blockDim.x) {
       const double x = s[c];
-      const double y = c + 1 < cols ? s[c + 1] : 0.0;
+      const double y = c + 1 < j.cols ? s[c + 1] : 0.0;
       d[c >> 1] = make_double2(x, y);  // ldd even and >= cols + (cols & 1): the pad column takes 0
     }
   }
 }
 
-int repitch(const double* src, int64_t lds, double* dst, int64_t ldd, int64_t rows, int64_t cols,
-            cudaStream_t stream) {
+// Re-pitch job j0 and, if j1.rows > 0, j1 too, in one launch.
+int repitch(const RepitchJob& j0, const RepitchJob& j1, cudaStream_t stream) {
+  const int64_t rows = std::max(j0.rows, j1.rows), cols = std::max(j0.cols, j1.cols);
   const int64_t pairs = (cols + 1) / 2;
   const unsigned gx = (unsigned)std::min<int64_t>((pairs + 255) / 256, 8);
   const unsigned gy = (unsigned)std::min<int64_t>(rows, 65535);
-  repitch_kernel<<<dim3(gx, gy), 256, 0, stream>>>(src, lds, dst, ldd, rows, cols);
+  repitch_kernel<<<dim3(gx, gy, j1.rows > 0 ? 2 : 1), 256, 0, stream>>>(j0, j1);
   TB_CUDA(cudaGetLastError(), "staging copy launch");
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return TB_STATUS_OK;
@@ -330,7 +342,11 @@ int launch(int dev, const double* A, int64_t lda, const double* B, int64_t ldb, 
   // two host threads on one stream cannot interleave repitch(A1), repitch(A2),
   // gemm1, gemm2 on the shared stream-keyed staging buffer.
   std::unique_lock<std::mutex> stage_lk(g_dev[dev].stage_mu, std::defer_lock);
-  if (variant == TB_VARIANT_AUTO && !tma_ok(A, lda, B, ldb) && 2.0 * (double)m * (double)n * (double)k >= kStageMinFlops) {
+  static const double stage_min = [] {  // TB_STAGE_MIN_FLOPS: A/B override of kStageMinFlops
+    const char* e = std::getenv("TB_STAGE_MIN_FLOPS");
+    return e ? std::atof(e) : kStageMinFlops;
+  }();
+  if (variant == TB_VARIANT_AUTO && !tma_ok(A, lda, B, ldb) && 2.0 * (double)m * (double)n * (double)k >= stage_min) {
     const bool sa = misaligned(A, lda), sb = misaligned(B, ldb);
     const int64_t lda2 = (k + 1) & ~int64_t(1), ldb2 = (n + 1) & ~int64_t(1);
     const size_t ea = sa ? (size_t)(m * lda2 + 32) : 0, eb = sb ? (size_t)(k * ldb2) : 0;
@@ -350,13 +366,13 @@ int launch(int dev, const double* A, int64_t lda, const double* B, int64_t ldb, 
       if ((s = stage_workspace(dev, stream, ea + eb + 32, &buf))) return s;
       double* a2 = buf;
       double* b2 = buf + ((ea + 31) & ~size_t(31));  // 256-byte aligned
+      const RepitchJob ja{A, lda, a2, lda2, m, k}, jb{B, ldb, b2, ldb2, k, n}, none{nullptr, 0, nullptr, 0, 0, 0};
+      if ((s = repitch(sa ? ja : jb, sa && sb ? jb : none, stream))) return s;
       if (sa) {
-        if ((s = repitch(A, lda, a2, lda2, m, k, stream))) return s;
         A = a2;
         lda = lda2;
       }
       if (sb) {
-        if ((s = repitch(B, ldb, b2, ldb2, k, n, stream))) return s;
         B = b2;
         ldb = ldb2;
       }

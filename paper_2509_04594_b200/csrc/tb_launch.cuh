@@ -277,28 +277,40 @@ struct RepitchJob {
   int64_t ldd, rows, cols;
 };
 
-// One launch re-pitches up to two operands (blockIdx.z picks the job).
+// One launch re-pitches up to two operands (blockIdx.z picks the job). Each
+// thread moves up to U pairs per step with all loads issued before the
+// stores (bytes in flight bound this HBM copy).
+template <int U>
 __global__ void __launch_bounds__(256) repitch_kernel(RepitchJob j0, RepitchJob j1) {
   const RepitchJob& j = blockIdx.z == 0 ? j0 : j1;
+  const int64_t pairs = (j.cols + 1) / 2;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t r = blockIdx.y; r < j.rows; r += gridDim.y) {
     const double* s = j.src + r * j.lds;
     double2* d = reinterpret_cast<double2*>(j.dst + r * j.ldd);
-    for (int64_t c = 2 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x); c < j.cols;
-         c += 2 * (int64_t)gridDim.x * blockDim.x) {
-      const double x = s[c];
-      const double y = c + 1 < j.cols ? s[c + 1] : 0.0;
-      d[c >> 1] = make_double2(x, y);  // ldd even and >= cols + (cols & 1): the pad column takes 0
+    for (int64_t p0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p0 < pairs; p0 += U * stride) {
+      double x[U], y[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t c = 2 * (p0 + u * stride);
+        x[u] = c < j.cols ? __ldg(s + c) : 0.0;
+        y[u] = c + 1 < j.cols ? __ldg(s + c + 1) : 0.0;  // ldd even, >= cols + (cols & 1): pad column 0
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (p0 + u * stride < pairs) d[p0 + u * stride] = make_double2(x[u], y[u]);
     }
   }
 }
 
 // Re-pitch job j0 and, if j1.rows > 0, j1 too, in one launch.
 int repitch(const RepitchJob& j0, const RepitchJob& j1, cudaStream_t stream) {
+  constexpr int U = 4;
   const int64_t rows = std::max(j0.rows, j1.rows), cols = std::max(j0.cols, j1.cols);
   const int64_t pairs = (cols + 1) / 2;
-  const unsigned gx = (unsigned)std::min<int64_t>((pairs + 255) / 256, 8);
+  const unsigned gx = (unsigned)std::min<int64_t>((pairs + 256 * U - 1) / (256 * U), 8);
   const unsigned gy = (unsigned)std::min<int64_t>(rows, 65535);
-  repitch_kernel<<<dim3(gx, gy, j1.rows > 0 ? 2 : 1), 256, 0, stream>>>(j0, j1);
+  repitch_kernel<U><<<dim3(gx, gy, j1.rows > 0 ? 2 : 1), 256, 0, stream>>>(j0, j1);
   TB_CUDA(cudaGetLastError(), "staging copy launch");
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return TB_STATUS_OK;

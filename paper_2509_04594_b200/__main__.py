@@ -7,7 +7,8 @@ Same flags (``--backends --sizes --trials --seed --tile --warmup --verify
 exit codes (0 ok, 1 trial failure with a ``# aborted:`` marker, 2 bad
 configuration; cli.py:110-135), so ``tilebench analyze --in <out>`` consumes
 the GPU rows unchanged. ``--verify`` compares the last trial of each pair with
-cuBLAS DGEMM on the device (normwise and max_abs_rel_diff bars).
+the host CPU product (numpy's BLAS; ``--verify-with cublas``: cuBLAS DGEMM on
+the device) against the reference's max_abs_rel_diff bar.
 """
 from __future__ import annotations
 
@@ -41,9 +42,21 @@ def build_parser() -> argparse.ArgumentParser:
     run.add_argument("--tile", type=int, default=32)
     run.add_argument("--warmup", type=int, default=1)
     run.add_argument("--verify", action="store_true", help="check the last product of each pair after timing")
+    run.add_argument("--verify-with", choices=("cpu", "cublas"), default="cpu",
+                     help="--verify reference: the host CPU product (numpy / BLAS, like the reference's CPU "
+                          "oracle check, harness.py:237-243) or cuBLAS DGEMM on the device")
     run.add_argument("--out", required=True, help="records CSV path")
     run.set_defaults(fn=cmd_run)
     return parser
+
+
+def _host_product(a, b):
+    """The CPU product of the trial's own operands (numpy's BLAS on the host):
+    an independent reference for ``--verify``, as the reference checks against
+    its CPU oracle; not this package's GPU code."""
+    import numpy as np
+
+    return np.matmul(np.asarray(a, dtype=np.float64), np.asarray(b, dtype=np.float64))
 
 
 def cmd_run(args) -> int:
@@ -61,8 +74,11 @@ def cmd_run(args) -> int:
         print(f"{name} n={n} trial {trial + 1}/{total}", file=sys.stderr)
 
     try:
+        verifier = None
+        if args.verify:
+            verifier = cublas_multiply if args.verify_with == "cublas" else _host_product
         records, meta = run_trials(config, registry, progress=progress, on_record=records.append,
-                                   verifier=cublas_multiply if args.verify else None)
+                                   verifier=verifier)
     except TrialError as exc:
         meta = RunMetadata.capture(config, {"clock": "cuda-events kernel-only"})
         write_records(args.out, records, meta, aborted=str(exc))

@@ -739,10 +739,13 @@ def test_cli_run_writes_reference_csv(tb, tmp_path):
 
     out = tmp_path / "gpu.csv"
     assert main(["run", "--backends", "gpu-tiled,cublas-dgemm", "--sizes", "64,200", "--trials", "2",
-                 "--verify", "--out", str(out)]) == 0
+                 "--verify", "--out", str(out)]) == 0  # host CPU product as the --verify reference
     lines = out.read_text().splitlines()
     assert lines[0] == "backend,n,trial,seconds,flops" and len(lines) == 1 + 2 * 2 * 2
     assert (tmp_path / "gpu.csv.meta.json").exists()
+    out2 = tmp_path / "gpu2.csv"
+    assert main(["run", "--backends", "gpu-tiled", "--sizes", "333", "--trials", "1", "--verify",
+                 "--verify-with", "cublas", "--out", str(out2)]) == 0
 
 
 def test_n32768_sampled_exact_oracle(tb, oracle):

@@ -500,7 +500,8 @@ def run_ours(args) -> None:
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": "dgemm_dmma_kernel<1, 6, TMA, DMMA, 128> (cross-stage prefetch) on the whole 128x128 "
-                                   "tiles + edge-strip launches for ragged m / n; achieved over the whole GEMM call",
+                                   "tiles + edge-strip launches for ragged m / n on a side stream filling its tail; "
+                                   "achieved over the whole GEMM call",
                          "flops_per_launch": flops_per_launch,
                          "avg_launch_ms": avg_launch * 1e3, "peak_source": peak_src},
             "e2e": {"value": flop_count(n) / e2e_s / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d,

@@ -237,3 +237,19 @@ def test_records_readable_by_reference_reader(tmp_path):
         sys.path.remove(str(copy / "src"))
         for k in [k for k in sys.modules if k == "tilebench" or k.startswith("tilebench.")]:
             del sys.modules[k]
+
+
+def test_cli_verify_reference_choice():
+    """--verify checks against the host CPU product by default (the reference's
+    CPU-oracle semantics, harness.py:237-243); --verify-with cublas keeps the
+    device check."""
+    import numpy as np
+
+    from paper_2509_04594_b200.__main__ import _host_product, build_parser
+
+    args = build_parser().parse_args(["run", "--sizes", "4", "--out", "x.csv", "--verify"])
+    assert args.verify and args.verify_with == "cpu"
+    args = build_parser().parse_args(["run", "--sizes", "4", "--out", "x.csv", "--verify", "--verify-with", "cublas"])
+    assert args.verify_with == "cublas"
+    a, b = np.arange(6.0).reshape(2, 3), np.arange(12.0).reshape(3, 4)
+    assert np.array_equal(_host_product(a, b), a @ b)
